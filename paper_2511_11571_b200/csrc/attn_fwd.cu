@@ -1,0 +1,401 @@
+// Forward: gather-and-densify over key blocks (moba_forward,
+// src/attention.py:147-182; paper Alg. 1), key-block-major.
+//
+// Work item = (head, key block j, 64-row tile of block j's varlen slice).
+// The CTA gathers the tile's query rows (flat_queries) into shared memory,
+// streams K_j / V_j, and runs S = Q K_j^T, the token-causal mask
+// (src/attention.py:127-133), an online softmax over 64-key chunks
+// (SoftmaxState.update, src/attention.py:60-68) and P V_j on the tensor
+// cores. Each (query, block) pair yields one partial (O_s normalised, bf16;
+// lse_s fp32) stored at its flat position; moba_combine merges a query's
+// partials into O and LSE (SoftmaxState.finalize, src/attention.py:70-74).
+//
+// This is the legacy-MMA (mma.sync m16n8k16) path.
+#include "common.cuh"
+
+namespace moba {
+
+constexpr int kFwdBM = 64;        // gathered query rows per item
+constexpr int kFwdThreads = 128;  // 4 warps x 16 rows
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct FwdItem {
+    int32_t hj;    // head * n_blocks + j
+    int32_t row0;  // first slice row of the tile
+};
+
+template <int D>
+struct FwdSmem {
+    static constexpr int RB = D * 2;  // bytes per bf16 row
+};
+
+// Q rows of the tile; K_j, V_j padded to BP rows (multiple of 64), zero filled.
+template <int D>
+__global__ void __launch_bounds__(kFwdThreads)
+moba_fwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                    const __nv_bfloat16* __restrict__ V, int64_t N, int B, int BP, int width,
+                    const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                    const int32_t* __restrict__ flat, const FwdItem* __restrict__ items,
+                    const int32_t* __restrict__ n_items_ptr, float scale_log2,
+                    __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse) {
+    constexpr int RB = D * 2;
+    constexpr int CH = D / 8;  // 16-byte chunks per row
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* q_s = smem;
+    uint8_t* k_s = q_s + kFwdBM * RB;
+    uint8_t* v_s = k_s + BP * RB;
+    int32_t* qid_s = reinterpret_cast<int32_t*>(v_s + BP * RB);
+
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int n_items = *n_items_ptr;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const FwdItem item = items[it];
+        const int64_t h = item.hj / n_blocks;
+        const int j = item.hj % n_blocks;
+        const int cnt = counts[item.hj];
+        const int rows = min(kFwdBM, cnt - item.row0);
+        const int64_t pbase = (int64_t)offsets[item.hj] + item.row0;  // head-local flat position
+        const int32_t* fl = flat + h * N * width + pbase;
+        const int64_t k0 = (int64_t)j * B;
+        const int klen = (int)min64(B, N - k0);
+        const __nv_bfloat16* Qh = Q + h * N * D;
+        const __nv_bfloat16* Kh = K + (h * N + k0) * D;
+        const __nv_bfloat16* Vh = V + (h * N + k0) * D;
+
+        __syncthreads();  // previous item's smem readers are done
+        if (tid < kFwdBM) qid_s[tid] = (tid < rows) ? fl[tid] : -1;
+        __syncthreads();
+        // gather Q rows (zero fill past the tile)
+        for (int e = tid; e < kFwdBM * CH; e += kFwdThreads) {
+            int r = e / CH, c = e % CH;
+            int qi = qid_s[r];
+            cp_async16(smem_u32(q_s + swz<RB>(r, c)), Qh + (int64_t)max(qi, 0) * D + c * 8, qi >= 0);
+        }
+        // K_j, V_j (zero fill past the block / sequence end)
+        for (int e = tid; e < BP * CH; e += kFwdThreads) {
+            int r = e / CH, c = e % CH;
+            bool ok = r < klen;
+            int rr = ok ? r : 0;
+            cp_async16(smem_u32(k_s + swz<RB>(r, c)), Kh + (int64_t)rr * D + c * 8, ok);
+            cp_async16(smem_u32(v_s + swz<RB>(r, c)), Vh + (int64_t)rr * D + c * 8, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+
+        const int m0 = warp * 16;
+        const int q_lo = qid_s[m0 + g];
+        const int q_hi = qid_s[m0 + g + 8];
+        // Q fragments for the whole d range
+        uint32_t qa[D / 16][4];
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+            int r = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+            int c = kk * 2 + (lane >> 4);
+            ldmatrix_x4(smem_u32(q_s + swz<RB>(r, c)), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+        }
+        float o[D / 8][4];
+#pragma unroll
+        for (int nt = 0; nt < D / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+        float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+        for (int kc = 0; kc < BP; kc += 64) {
+            float s[8][4];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+                for (int np = 0; np < 4; ++np) {  // pairs of n-tiles (16 keys)
+                    int key = kc + np * 16 + (lane & 7) + (lane >> 4) * 8;
+                    int c = kk * 2 + ((lane >> 3) & 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldmatrix_x4(smem_u32(k_s + swz<RB>(key, c)), b0, b1, b2, b3);
+                    mma_bf16_16816(s[2 * np], qa[kk], b0, b1);
+                    mma_bf16_16816(s[2 * np + 1], qa[kk], b2, b3);
+                }
+            }
+            // scale into the log2 domain and mask: key col c valid iff
+            // c < klen and k0 + c <= query
+            float cm_lo = -INFINITY, cm_hi = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    int col = kc + nt * 8 + 2 * t4 + (e & 1);
+                    int qq = (e < 2) ? q_lo : q_hi;
+                    bool ok = col < klen && (k0 + col) <= (int64_t)qq;
+                    float v = ok ? s[nt][e] * scale_log2 : -INFINITY;
+                    s[nt][e] = v;
+                    if (e < 2) cm_lo = fmaxf(cm_lo, v); else cm_hi = fmaxf(cm_hi, v);
+                }
+            }
+            cm_lo = fmaxf(cm_lo, __shfl_xor_sync(0xffffffffu, cm_lo, 1));
+            cm_lo = fmaxf(cm_lo, __shfl_xor_sync(0xffffffffu, cm_lo, 2));
+            cm_hi = fmaxf(cm_hi, __shfl_xor_sync(0xffffffffu, cm_hi, 1));
+            cm_hi = fmaxf(cm_hi, __shfl_xor_sync(0xffffffffu, cm_hi, 2));
+            float mn_lo = fmaxf(m_lo, cm_lo), mn_hi = fmaxf(m_hi, cm_hi);
+            // rows with no visible key yet keep a finite reference point
+            float ref_lo = (mn_lo == -INFINITY) ? 0.f : mn_lo;
+            float ref_hi = (mn_hi == -INFINITY) ? 0.f : mn_hi;
+            float al_lo = fast_exp2(m_lo - ref_lo), al_hi = fast_exp2(m_hi - ref_hi);
+            m_lo = mn_lo;
+            m_hi = mn_hi;
+            l_lo *= al_lo;
+            l_hi *= al_hi;
+#pragma unroll
+            for (int nt = 0; nt < D / 8; ++nt) {
+                o[nt][0] *= al_lo;
+                o[nt][1] *= al_lo;
+                o[nt][2] *= al_hi;
+                o[nt][3] *= al_hi;
+            }
+            uint32_t pa[4][4];  // P as A fragments, 4 k16 slices
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                float p0 = fast_exp2(s[nt][0] - ref_lo);
+                float p1 = fast_exp2(s[nt][1] - ref_lo);
+                float p2 = fast_exp2(s[nt][2] - ref_hi);
+                float p3 = fast_exp2(s[nt][3] - ref_hi);
+                l_lo += p0 + p1;
+                l_hi += p2 + p3;
+                pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+                pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+            }
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+                for (int np = 0; np < D / 16; ++np) {
+                    int key = kc + ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+                    int c = np * 2 + (lane >> 4);
+                    uint32_t b0, b1, b2, b3;
+                    ldmatrix_x4_trans(smem_u32(v_s + swz<RB>(key, c)), b0, b1, b2, b3);
+                    mma_bf16_16816(o[2 * np], pa[ks], b0, b1);
+                    mma_bf16_16816(o[2 * np + 1], pa[ks], b2, b3);
+                }
+            }
+        }
+        l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 1);
+        l_lo += __shfl_xor_sync(0xffffffffu, l_lo, 2);
+        l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 1);
+        l_hi += __shfl_xor_sync(0xffffffffu, l_hi, 2);
+        const float inv_lo = 1.f / l_lo, inv_hi = 1.f / l_hi;
+        __nv_bfloat16* po = part_o + (h * N * width + pbase) * D;
+        float* pl = part_lse + h * N * width + pbase;
+        const int r_lo = m0 + g, r_hi = m0 + g + 8;
+#pragma unroll
+        for (int nt = 0; nt < D / 8; ++nt) {
+            int col = nt * 8 + 2 * t4;
+            if (r_lo < rows)
+                *reinterpret_cast<uint32_t*>(po + (int64_t)r_lo * D + col) =
+                    pack_bf16(o[nt][0] * inv_lo, o[nt][1] * inv_lo);
+            if (r_hi < rows)
+                *reinterpret_cast<uint32_t*>(po + (int64_t)r_hi * D + col) =
+                    pack_bf16(o[nt][2] * inv_hi, o[nt][3] * inv_hi);
+        }
+        if (t4 == 0) {
+            if (r_lo < rows) pl[r_lo] = (m_lo + __log2f(l_lo)) * kLn2;
+            if (r_hi < rows) pl[r_hi] = (m_hi + __log2f(l_hi)) * kLn2;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- combine
+// One warp per query: merge its <= width partials (lse-weighted).
+template <int D>
+__global__ void moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_lse,
+                                    const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t total_rows,
+                                    __nv_bfloat16* __restrict__ O, float* __restrict__ LSE) {
+    constexpr int PER = D / 32;  // channels per lane
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= total_rows) return;
+    const int64_t h = row / N;
+    const int32_t* rp = row_pos + row * width;
+    int32_t p = (lane < width) ? rp[lane] : -1;
+    float ls = (p >= 0) ? part_lse[h * N * width + p] : -INFINITY;
+    float m = warp_max(ls);
+    float w = (p >= 0) ? __expf(ls - m) : 0.f;
+    float wsum = warp_sum(w);
+    float acc[PER];
+#pragma unroll
+    for (int c = 0; c < PER; ++c) acc[c] = 0.f;
+    for (int s = 0; s < width; ++s) {
+        int32_t ps = __shfl_sync(0xffffffffu, p, s);
+        float ws = __shfl_sync(0xffffffffu, w, s);
+        if (ps < 0) continue;
+        const __nv_bfloat16* src = part_o + (h * N * width + ps) * D + lane * PER;
+        if constexpr (PER == 2) {
+            float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(src));
+            acc[0] = fmaf(ws, f.x, acc[0]);
+            acc[1] = fmaf(ws, f.y, acc[1]);
+        } else {
+            uint2 u = *reinterpret_cast<const uint2*>(src);
+            float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y);
+            acc[0] = fmaf(ws, f0.x, acc[0]);
+            acc[1] = fmaf(ws, f0.y, acc[1]);
+            acc[2] = fmaf(ws, f1.x, acc[2]);
+            acc[3] = fmaf(ws, f1.y, acc[3]);
+        }
+    }
+    const float inv = 1.f / wsum;
+    __nv_bfloat16* dst = O + row * D + lane * PER;
+    if constexpr (PER == 2) {
+        *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
+    } else {
+        *reinterpret_cast<uint2*>(dst) =
+            make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+    }
+    if (lane == 0) LSE[row] = m + __logf(wsum);
+}
+
+// ---------------------------------------------------------------- work items
+// One thread per (head, block): exclusive scan of tile counts in a single
+// CTA, then each (head, block) writes its items.
+__global__ void __launch_bounds__(1024)
+fwd_items_scan_kernel(const int32_t* __restrict__ counts, int64_t total, int bm, int32_t* __restrict__ item_off,
+                      int32_t* __restrict__ n_items) {
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < total; b0 += 1024) {
+        int64_t b = b0 + threadIdx.x;
+        int32_t v = (b < total) ? (counts[b] + bm - 1) / bm : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int32_t t = warp_tot[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        if (b < total) item_off[b] = carry + (wid ? warp_tot[wid - 1] : 0) + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += warp_tot[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_items = carry;
+}
+
+__global__ void fwd_items_fill_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ item_off,
+                                      int64_t total, int bm, FwdItem* __restrict__ items) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= total) return;
+    int nt = (counts[b] + bm - 1) / bm;
+    int32_t o = item_off[b];
+    for (int t = 0; t < nt; ++t) items[o + t] = FwdItem{(int32_t)b, t * bm};
+}
+
+// workspace layout (all head-local regions back to back):
+//   part_o   bf16 [bh, N*width, D]
+//   part_lse f32  [bh, N*width]
+//   item_off i32  [bh*n]
+//   n_items  i32
+//   items    FwdItem [bh*(ceil(N*width/BM) + n)]
+struct FwdWs {
+    size_t part_o, part_lse, item_off, n_items, items, total;
+};
+
+static FwdWs fwd_ws_layout(int64_t bh, int64_t N, int D, int B, int width) {
+    FwdWs w;
+    int64_t n = ceil_div(N, B);
+    int64_t E = N * width;
+    size_t off = 0;
+    w.part_o = off;
+    off = align_up(off + (size_t)bh * E * D * 2, 256);
+    w.part_lse = off;
+    off = align_up(off + (size_t)bh * E * 4, 256);
+    w.item_off = off;
+    off = align_up(off + (size_t)bh * n * 4, 256);
+    w.n_items = off;
+    off = align_up(off + 4, 256);
+    w.items = off;
+    off = align_up(off + (size_t)bh * (ceil_div(E, kFwdBM) + n) * sizeof(FwdItem), 256);
+    w.total = off;
+    return w;
+}
+
+template <int D>
+static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
+                      const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* row_pos,
+                      float scale, void* out, float* lse, uint8_t* ws, const FwdWs& L, cudaStream_t s) {
+    const int64_t n = ceil_div(N, B);
+    const int64_t total = bh * n;
+    int32_t* item_off = (int32_t*)(ws + L.item_off);
+    int32_t* n_items = (int32_t*)(ws + L.n_items);
+    FwdItem* items = (FwdItem*)(ws + L.items);
+    fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, kFwdBM, item_off, n_items);
+    fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, kFwdBM, items);
+    int st = check_launch("fwd_items", 2);
+    if (st) return st;
+    const int BP = (int)ceil_div(B, 64) * 64;
+    const size_t smem = (size_t)(kFwdBM + 2 * BP) * D * 2 + kFwdBM * 4;
+    auto kern = moba_fwd_mma_kernel<D>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFwdThreads, smem);
+    if (occ < 1) return MOBA_ERR_UNSUPPORTED;
+    const int64_t max_items = bh * (ceil_div(N * width, kFwdBM) + n);
+    const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs * occ);
+    {
+    StageTimer tm(T_FWD, s);
+    kern<<<grid, kFwdThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                         (const __nv_bfloat16*)v, N, B, BP, width, counts, offsets, flat, items,
+                                         n_items, scale * kLog2e, (__nv_bfloat16*)(ws + L.part_o),
+                                         (float*)(ws + L.part_lse));
+    }
+    st = check_launch("moba_fwd_mma_kernel");
+    if (st) return st;
+    StageTimer tm(T_COMBINE, s);
+    const int64_t rows = bh * N;
+    moba_combine_kernel<D><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(
+        (const __nv_bfloat16*)(ws + L.part_o), (const float*)(ws + L.part_lse), row_pos, N, width, rows,
+        (__nv_bfloat16*)out, lse);
+    return check_launch("moba_combine_kernel");
+}
+
+}  // namespace moba
+
+using namespace moba;
+
+extern "C" size_t moba_fwd_workspace_size(int64_t bh, int64_t n_tokens, int head_dim, int block_size, int width) {
+    if (bh < 1 || n_tokens < 1 || block_size < 1 || width < 1) return 0;
+    return fwd_ws_layout(bh, n_tokens, head_dim, block_size, width).total;
+}
+
+extern "C" int moba_fwd(const void* q, const void* k, const void* v, int64_t bh, int64_t n_tokens, int head_dim,
+                        int block_size, int width, const int32_t* counts, const int32_t* offsets,
+                        const int32_t* flat, const int32_t* row_pos, float softmax_scale, void* out, float* lse,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+    if (bh < 1 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
+    if (width > 32 || block_size > 256) return MOBA_ERR_UNSUPPORTED;
+    if (n_tokens * width >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
+    FwdWs L = fwd_ws_layout(bh, n_tokens, head_dim, block_size, width);
+    if (workspace_bytes < L.total) return MOBA_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = (uint8_t*)workspace;
+    if (head_dim == 64)
+        return launch_fwd<64>(q, k, v, bh, n_tokens, block_size, width, counts, offsets, flat, row_pos,
+                              softmax_scale, out, lse, ws, L, s);
+    if (head_dim == 128)
+        return launch_fwd<128>(q, k, v, bh, n_tokens, block_size, width, counts, offsets, flat, row_pos,
+                               softmax_scale, out, lse, ws, L, s);
+    return MOBA_ERR_UNSUPPORTED;
+}

@@ -1,0 +1,204 @@
+// Stage 1: key-block centroids, optionally fused with the causal key
+// short-conv (src/router.py:32-46, src/keyconv.py:59-78).
+//
+// One CTA per (head, key block). HBM-bound: reads the block's K rows once
+// (the width-1 halo rows above the block come from L2), writes K' (bf16)
+// when the conv is on, and one fp32 centroid row.
+#include "common.cuh"
+
+namespace moba {
+
+constexpr int kCentThreads = 256;
+constexpr int kMaxConv = 5;
+
+__device__ __forceinline__ float sigmoidf_acc(float x) {
+    // overflow-safe two-branch form, as src/keyconv.py:50-56
+    float e = expf(-fabsf(x));
+    return x >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+}
+
+__global__ void __launch_bounds__(kCentThreads)
+centroid_conv_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W, int width,
+                     int64_t N, int D, int B, __nv_bfloat16* __restrict__ Kout,
+                     float* __restrict__ cent) {
+    extern __shared__ float red[];  // [row_groups][D]
+    const int j = blockIdx.x;
+    const int64_t h = blockIdx.y;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int CG = D / 8;                 // 16-byte column groups
+    const int RG = kCentThreads / CG;     // row groups
+    const int cg = threadIdx.x % CG;
+    const int rg = threadIdx.x / CG;
+    const int64_t t0 = (int64_t)j * B;
+    const int len = (int)min64(B, N - t0);
+    const __nv_bfloat16* Kh = K + h * N * D;
+
+    float w[kMaxConv][8];
+#pragma unroll
+    for (int l = 0; l < kMaxConv; ++l)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) w[l][c] = (l < width) ? W[l * D + cg * 8 + c] : 0.f;
+
+    float acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+
+    for (int r = rg; r < len; r += RG) {
+        const int64_t t = t0 + r;
+        uint4 raw = *reinterpret_cast<const uint4*>(Kh + t * D + cg * 8);
+        float x[8];
+        {
+            const uint32_t* u = reinterpret_cast<const uint32_t*>(&raw);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float2 f = unpack_bf16(u[c]);
+                x[2 * c] = f.x;
+                x[2 * c + 1] = f.y;
+            }
+        }
+        if (width > 0) {
+            float a[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) a[c] = w[0][c] * x[c];
+#pragma unroll
+            for (int l = 1; l < kMaxConv; ++l) {
+                if (l < width && t - l >= 0) {
+                    uint4 rr = *reinterpret_cast<const uint4*>(Kh + (t - l) * D + cg * 8);
+                    const uint32_t* u = reinterpret_cast<const uint32_t*>(&rr);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float2 f = unpack_bf16(u[c]);
+                        a[2 * c] = fmaf(w[l][2 * c], f.x, a[2 * c]);
+                        a[2 * c + 1] = fmaf(w[l][2 * c + 1], f.y, a[2 * c + 1]);
+                    }
+                }
+            }
+            uint32_t o[4];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = x[c] + a[c] * sigmoidf_acc(a[c]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) o[c] = pack_bf16(x[2 * c], x[2 * c + 1]);
+            *reinterpret_cast<uint4*>(Kout + h * N * D + t * D + cg * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] += x[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) red[rg * D + cg * 8 + c] = acc[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < D; c += kCentThreads) {
+        float s = 0.f;
+        for (int g = 0; g < RG; ++g) s += red[g * D + c];
+        cent[(h * n_blocks + j) * D + c] = s / (float)len;
+    }
+}
+
+// ---------------------------------------------------------------- conv backward
+// key_conv_backward (src/keyconv.py:81-104). One CTA per (head, 64-row
+// chunk): g over the chunk plus a (width-1)-row lookahead in smem, then
+// dK_t = dK'_t + sum_l W[l] g_{t+l}; per-CTA dW partials reduced by a
+// second kernel (deterministic, no atomics).
+constexpr int kConvRows = 64;
+
+__global__ void __launch_bounds__(256)
+conv_bwd_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W, int width,
+                const __nv_bfloat16* __restrict__ dKc, int64_t N, int D,
+                __nv_bfloat16* __restrict__ dK, float* __restrict__ dw_part) {
+    extern __shared__ float g_s[];  // [(kConvRows + kMaxConv - 1)][D]
+    const int64_t h = blockIdx.y;
+    const int64_t t0 = (int64_t)blockIdx.x * kConvRows;
+    const __nv_bfloat16* Kh = K + h * N * D;
+    const __nv_bfloat16* dKch = dKc + h * N * D;
+    const int rows = kConvRows + width - 1;
+    for (int e = threadIdx.x; e < rows * D; e += blockDim.x) {
+        int r = e / D, c = e % D;
+        int64_t t = t0 + r;
+        float g = 0.f;
+        if (t < N) {
+            float a = 0.f;
+            for (int l = 0; l < width; ++l)
+                if (t - l >= 0) a = fmaf(W[l * D + c], __bfloat162float(Kh[(t - l) * D + c]), a);
+            float s = sigmoidf_acc(a);
+            g = __bfloat162float(dKch[t * D + c]) * (s * (1.f + a * (1.f - s)));
+        }
+        g_s[r * D + c] = g;
+    }
+    __syncthreads();
+    // dK and dW partial: thread owns channel c, loops rows
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        float dwl[kMaxConv] = {0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int r = 0; r < kConvRows; ++r) {
+            int64_t t = t0 + r;
+            if (t >= N) break;
+            float v = __bfloat162float(dKch[t * D + c]);
+            for (int l = 0; l < width; ++l) v = fmaf(W[l * D + c], g_s[(r + l) * D + c], v);
+            dK[h * N * D + t * D + c] = __float2bfloat16(v);
+            float gt = g_s[r * D + c];
+            for (int l = 0; l < width; ++l)
+                if (t - l >= 0) dwl[l] = fmaf(gt, __bfloat162float(Kh[(t - l) * D + c]), dwl[l]);
+        }
+        int64_t part = h * gridDim.x + blockIdx.x;
+        for (int l = 0; l < width; ++l) dw_part[(part * width + l) * D + c] = dwl[l];
+    }
+}
+
+__global__ void conv_dw_reduce_kernel(const float* __restrict__ dw_part, int64_t n_parts, int width, int D,
+                                      float* __restrict__ dw) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= width * D) return;
+    float s = 0.f;
+    for (int64_t p = 0; p < n_parts; ++p) s += dw_part[p * width * D + e];
+    dw[e] = s;
+}
+
+}  // namespace moba
+
+using namespace moba;
+
+extern "C" int moba_centroids(const void* k, const float* conv_w, int conv_width, int64_t bh,
+                              int64_t n_tokens, int head_dim, int block_size, void* k_conv_out,
+                              float* centroids, void* stream) {
+    if (bh < 1 || n_tokens < 1 || block_size < 1) return MOBA_ERR_SHAPE;
+    if (head_dim % 8 != 0 || head_dim > 256) return MOBA_ERR_UNSUPPORTED;
+    if (conv_width < 0 || conv_width > kMaxConv) return MOBA_ERR_CONFIG;
+    if (conv_width > 0 && (conv_w == nullptr || k_conv_out == nullptr)) return MOBA_ERR_CONFIG;
+    const int64_t n_blocks = ceil_div(n_tokens, block_size);
+    if (n_blocks > 2147483647 || bh > 65535) return MOBA_ERR_UNSUPPORTED;
+    dim3 grid((unsigned)n_blocks, (unsigned)bh);
+    const int RG = kCentThreads / (head_dim / 8);
+    size_t smem = (size_t)RG * head_dim * sizeof(float);
+    StageTimer tm(T_CENTROID, (cudaStream_t)stream);
+    centroid_conv_kernel<<<grid, kCentThreads, smem, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)k, conv_w, conv_width, n_tokens, head_dim, block_size,
+        (__nv_bfloat16*)k_conv_out, centroids);
+    return check_launch("centroid_conv_kernel");
+}
+
+extern "C" size_t moba_conv_bwd_workspace_size(int64_t bh, int64_t n_tokens, int head_dim, int conv_width) {
+    return (size_t)bh * ceil_div(n_tokens, kConvRows) * conv_width * head_dim * sizeof(float);
+}
+
+extern "C" int moba_conv_bwd(const void* k, const float* conv_w, int conv_width, const void* dk_conv,
+                             int64_t bh, int64_t n_tokens, int head_dim, void* dk, float* dw,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+    if (bh < 1 || n_tokens < 1 || head_dim < 1) return MOBA_ERR_SHAPE;
+    if (conv_width < 1 || conv_width > kMaxConv) return MOBA_ERR_CONFIG;
+    if (workspace_bytes < moba_conv_bwd_workspace_size(bh, n_tokens, head_dim, conv_width))
+        return MOBA_ERR_WORKSPACE;
+    dim3 grid((unsigned)ceil_div(n_tokens, kConvRows), (unsigned)bh);
+    size_t smem = (size_t)(kConvRows + conv_width - 1) * head_dim * sizeof(float);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(conv_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    StageTimer tm(T_CONV_BWD, s);
+    conv_bwd_kernel<<<grid, 256, smem, s>>>((const __nv_bfloat16*)k, conv_w, conv_width,
+                                            (const __nv_bfloat16*)dk_conv, n_tokens, head_dim,
+                                            (__nv_bfloat16*)dk, (float*)workspace);
+    int st = check_launch("conv_bwd_kernel");
+    if (st) return st;
+    int e = conv_width * head_dim;
+    conv_dw_reduce_kernel<<<(e + 127) / 128, 128, 0, s>>>((const float*)workspace, bh * grid.x,
+                                                           conv_width, head_dim, dw);
+    return check_launch("conv_dw_reduce_kernel");
+}

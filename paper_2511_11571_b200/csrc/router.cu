@@ -1,0 +1,548 @@
+// Stages 2+3: tiled top-k routing and the key-block-major varlen plan.
+//
+//   select_topk  (src/router.py:49-120)   -> route_topk_fp32_kernel
+//   build_varlen (src/router.py:123-154)  -> varlen_count / varlen_scan /
+//                                            varlen_scatter kernels
+//   validate_plan (src/core.py:254-296)   -> validate_* kernels
+//
+// The router never materialises the [N, n] score matrix: a CTA holds 128
+// queries, streams 32-centroid chunks through shared memory, computes a
+// 128x32 fp32 score tile with register-blocked FFMA (exact fp32 products of
+// bf16 queries and fp32 centroids, summed in d order), and each thread keeps
+// its query's running top-k list in registers.
+#include "common.cuh"
+
+namespace moba {
+
+constexpr int kRouteQ = 128;    // queries per CTA (one per thread in selection)
+constexpr int kRouteC = 32;     // centroids per chunk
+constexpr int kRouteThreads = 128;
+
+// Insert candidate (s, j) into a list sorted by (score desc, index asc).
+// Candidates arrive in ascending j, so a tie with an existing entry keeps
+// the existing (lower-index) entry first: ties -> lower block index
+// (src/router.py:95-98). The displaced entries bubble down with the same
+// (score, index) order so equal scores stay index-ordered.
+template <int KMAX>
+MOBA_DEV void topk_insert(float (&ts)[KMAX], int (&ti)[KMAX], float s, int j) {
+    float cs = s;
+    int ci = j;
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        bool sw = (cs > ts[u]) || (cs == ts[u] && ci < ti[u]);
+        float t = ts[u];
+        int tt = ti[u];
+        ts[u] = sw ? cs : t;
+        ti[u] = sw ? ci : tt;
+        cs = sw ? t : cs;
+        ci = sw ? tt : ci;
+    }
+}
+
+template <int D, int KMAX>
+__global__ void __launch_bounds__(kRouteThreads)
+route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, int64_t N,
+                       int B, int top_k, int32_t* __restrict__ topk) {
+    extern __shared__ __align__(16) float route_smem[];
+    float (*q_s)[kRouteQ] = reinterpret_cast<float (*)[kRouteQ]>(route_smem);
+    float (*c_s)[kRouteC] = reinterpret_cast<float (*)[kRouteC]>(route_smem + D * kRouteQ);
+    float (*s_s)[kRouteC + 1] = reinterpret_cast<float (*)[kRouteC + 1]>(route_smem + D * (kRouteQ + kRouteC));
+
+    const int tid = threadIdx.x;
+    const int64_t h = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * kRouteQ;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int width = top_k + 1;
+    const __nv_bfloat16* Qh = Q + h * N * D;
+    const float* Ch = cent + (int64_t)h * n_blocks * D;
+
+    // stage the query tile transposed (fp32, exact)
+    for (int e = tid; e < kRouteQ * (D / 8); e += kRouteThreads) {
+        int r = e / (D / 8), cg = e % (D / 8);
+        int64_t i = r0 + r;
+        float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (i < N) {
+            uint4 raw = *reinterpret_cast<const uint4*>(Qh + i * D + cg * 8);
+            const uint32_t* u = reinterpret_cast<const uint32_t*>(&raw);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float2 f = unpack_bf16(u[c]);
+                x[2 * c] = f.x;
+                x[2 * c + 1] = f.y;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) q_s[cg * 8 + c][r] = x[c];
+    }
+
+    const int64_t my_i = r0 + tid;
+    const int my_own = (int)(min64(my_i, N - 1) / B);
+    const int64_t last_i = min64(r0 + kRouteQ, N) - 1;
+    const int max_own = (int)(last_i / B);
+
+    float ts[KMAX];
+    int ti[KMAX];
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        ts[u] = -INFINITY;
+        ti[u] = 0x7fffffff;
+    }
+
+    // micro-tile: 4 queries x 8 centroids per thread
+    const int qg = tid % 32;    // query group -> rows qg*4 .. +3
+    const int cgp = tid / 32;   // centroid group -> cols cgp*8 .. +7 (warp-uniform)
+
+    for (int c0 = 0; c0 < max_own; c0 += kRouteC) {
+        __syncthreads();  // previous chunk's c_s / s_s readers are done
+        for (int e = tid; e < kRouteC * D; e += kRouteThreads) {
+            int c = e / D, dd = e % D;
+            int j = c0 + c;
+            c_s[dd][c] = (j < n_blocks) ? Ch[(int64_t)j * D + dd] : 0.f;
+        }
+        __syncthreads();
+        float acc[4][8];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+#pragma unroll 8
+        for (int dd = 0; dd < D; ++dd) {
+            float4 qv = *reinterpret_cast<const float4*>(&q_s[dd][qg * 4]);
+            float4 c0v = *reinterpret_cast<const float4*>(&c_s[dd][cgp * 8]);
+            float4 c1v = *reinterpret_cast<const float4*>(&c_s[dd][cgp * 8 + 4]);
+            float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+            float cb[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(qa[a], cb[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) s_s[qg * 4 + a][cgp * 8 + b] = acc[a][b];
+        __syncthreads();
+        // selection: thread tid owns query r0 + tid; only strictly-past
+        // blocks j < own compete (src/router.py:92)
+        int lim = min(kRouteC, my_own - c0);
+        if (my_i < N) {
+            for (int c = 0; c < lim; ++c) {
+                float s = s_s[tid][c];
+                if (s > ts[KMAX - 1]) topk_insert<KMAX>(ts, ti, s, c0 + c);
+            }
+        }
+    }
+
+    if (my_i >= N) return;
+    // keep the first top_k entries, sort indices ascending, append own block
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u)
+        if (u >= top_k) ti[u] = 0x7fffffff;
+#pragma unroll
+    for (int p = 0; p < KMAX; ++p) {
+#pragma unroll
+        for (int u = (p & 1); u + 1 < KMAX; u += 2) {
+            int a = ti[u], b = ti[u + 1];
+            ti[u] = min(a, b);
+            ti[u + 1] = max(a, b);
+        }
+    }
+    int32_t* row = topk + (h * N + my_i) * width;
+    int nvalid = 0;
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        if (ti[u] != 0x7fffffff) {
+            row[u] = ti[u];
+            ++nvalid;
+        }
+    }
+    row[nvalid] = my_own;
+    for (int s = nvalid + 1; s < width; ++s) row[s] = -1;
+}
+
+// ---------------------------------------------------------------- varlen
+// build_varlen as a stable counting sort over query chunks:
+//  count   : per (head, chunk of TQ queries) a shared-memory histogram over
+//            blocks -> cc[h][chunk][b]
+//  scan    : per (head, block) exclusive scan over chunks (in place) and
+//            counts[b]; then offsets = exclusive scan over blocks
+//  scatter : per (head, chunk) one warp walks its queries in ascending
+//            order, lanes = row slots; a row never repeats a block, so the
+//            per-block cursors in shared memory are conflict free and each
+//            block's slice comes out strictly ascending (src/router.py:145-148).
+
+__global__ void varlen_count_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int n_blocks,
+                                    int TQ, int n_chunks, int32_t* __restrict__ cc, int* __restrict__ err) {
+    extern __shared__ int hist[];
+    const int64_t h = blockIdx.y;
+    const int chunk = blockIdx.x;
+    for (int b = threadIdx.x; b < n_blocks; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int64_t i0 = (int64_t)chunk * TQ;
+    const int64_t i1 = min64(i0 + TQ, N);
+    const int32_t* base = topk + h * N * width;
+    for (int64_t e = i0 * width + threadIdx.x; e < i1 * width; e += blockDim.x) {
+        int b = base[e];
+        if (b >= n_blocks || b < -1) {
+            atomicOr(err, 1);
+        } else if (b >= 0) {
+            atomicAdd(&hist[b], 1);
+        }
+    }
+    __syncthreads();
+    int32_t* out = cc + (h * n_chunks + chunk) * (int64_t)n_blocks;
+    for (int b = threadIdx.x; b < n_blocks; b += blockDim.x) out[b] = hist[b];
+}
+
+__global__ void __launch_bounds__(1024)
+varlen_scan_kernel(int32_t* __restrict__ cc, int n_blocks, int n_chunks, int32_t* __restrict__ counts,
+                   int32_t* __restrict__ offsets) {
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t carry;
+    const int64_t h = blockIdx.x;
+    int32_t* cch = cc + h * (int64_t)n_chunks * n_blocks;
+    // per block: exclusive scan over chunks
+    for (int b = threadIdx.x; b < n_blocks; b += blockDim.x) {
+        int32_t run = 0;
+        int c = 0;
+        for (; c + 4 <= n_chunks; c += 4) {
+            int32_t v0 = cch[(int64_t)(c + 0) * n_blocks + b];
+            int32_t v1 = cch[(int64_t)(c + 1) * n_blocks + b];
+            int32_t v2 = cch[(int64_t)(c + 2) * n_blocks + b];
+            int32_t v3 = cch[(int64_t)(c + 3) * n_blocks + b];
+            cch[(int64_t)(c + 0) * n_blocks + b] = run;
+            run += v0;
+            cch[(int64_t)(c + 1) * n_blocks + b] = run;
+            run += v1;
+            cch[(int64_t)(c + 2) * n_blocks + b] = run;
+            run += v2;
+            cch[(int64_t)(c + 3) * n_blocks + b] = run;
+            run += v3;
+        }
+        for (; c < n_chunks; ++c) {
+            int32_t v = cch[(int64_t)c * n_blocks + b];
+            cch[(int64_t)c * n_blocks + b] = run;
+            run += v;
+        }
+        counts[h * n_blocks + b] = run;
+    }
+    __syncthreads();
+    // offsets: exclusive scan of counts over blocks, 1024 at a time
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < n_blocks; b0 += 1024) {
+        int b = b0 + threadIdx.x;
+        int32_t v = (b < n_blocks) ? counts[h * n_blocks + b] : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int32_t t = warp_tot[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_tot[lane] = t;  // inclusive
+        }
+        __syncthreads();
+        int32_t excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - v;
+        if (b < n_blocks) offsets[h * n_blocks + b] = excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += warp_tot[31];
+        __syncthreads();
+    }
+}
+
+constexpr int kScatterBatch = 8;
+
+__global__ void __launch_bounds__(32)
+varlen_scatter_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int n_blocks, int TQ,
+                      int n_chunks, const int32_t* __restrict__ cc, const int32_t* __restrict__ offsets,
+                      int32_t* __restrict__ flat, int32_t* __restrict__ row_pos) {
+    extern __shared__ int32_t cursor[];
+    const int64_t h = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int lane = threadIdx.x;
+    const int32_t* ccc = cc + (h * n_chunks + chunk) * (int64_t)n_blocks;
+    for (int b = lane; b < n_blocks; b += 32) cursor[b] = offsets[h * n_blocks + b] + ccc[b];
+    __syncwarp();
+    const int64_t i0 = (int64_t)chunk * TQ;
+    const int64_t i1 = min64(i0 + TQ, N);
+    const int32_t* tk = topk + h * N * width;
+    int32_t* rp = row_pos + h * N * width;
+    int32_t* fl = flat + h * N * width;
+    // width <= 32: lane = slot, so one pass per query batch keeps the
+    // ascending-query order of every block's slice
+    for (int64_t ib = i0; ib < i1; ib += kScatterBatch) {
+        {
+            const int s = lane;
+            int32_t blk[kScatterBatch];
+#pragma unroll
+            for (int u = 0; u < kScatterBatch; ++u)
+                blk[u] = (ib + u < i1 && s < width) ? tk[(ib + u) * width + s] : -1;
+#pragma unroll
+            for (int u = 0; u < kScatterBatch; ++u) {
+                if (ib + u < i1) {
+                    int32_t b = blk[u];
+                    if (b >= 0) {
+                        int32_t p = cursor[b];
+                        cursor[b] = p + 1;
+                        fl[p] = (int32_t)(ib + u);
+                        rp[(ib + u) * width + s] = p;
+                    } else if (s < width) {
+                        rp[(ib + u) * width + s] = -1;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+}
+
+// row_pos from an arbitrary (validated) plan: binary search of query i in
+// block b's ascending slice.
+__global__ void plan_row_pos_kernel(const int32_t* __restrict__ topk, const int32_t* __restrict__ counts,
+                                    const int32_t* __restrict__ offsets, const int32_t* __restrict__ flat,
+                                    int64_t N, int width, int n_blocks, int32_t* __restrict__ row_pos) {
+    const int64_t h = blockIdx.y;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * width) return;
+    const int64_t i = e / width;
+    int32_t b = topk[h * N * width + e];
+    int32_t p = -1;
+    if (b >= 0) {
+        const int32_t* sl = flat + h * N * width + offsets[h * n_blocks + b];
+        int lo = 0, hi = counts[h * n_blocks + b];
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (sl[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        if (lo < counts[h * n_blocks + b] && sl[lo] == i) p = offsets[h * n_blocks + b] + lo;
+    }
+    row_pos[h * N * width + e] = p;
+}
+
+// ---------------------------------------------------------------- validation
+// flags: bit0 range, bit1 causality, bit2 duplicate, bit3 prefix/total,
+// bit4 slice order / range, bit5 (query, block) of topk absent from flat
+__global__ void validate_rows_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int B,
+                                     int n_blocks, unsigned long long* __restrict__ valid_count,
+                                     int* __restrict__ flags) {
+    const int64_t h = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int32_t* row = topk + (h * N + i) * width;
+    int nv = 0, f = 0;
+    const int own = (int)(i / B);
+    for (int s = 0; s < width; ++s) {
+        int b = row[s];
+        if (b < -1 || b >= n_blocks) f |= 1;
+        if (b >= 0) {
+            ++nv;
+            if (b > own) f |= 2;
+            for (int t = 0; t < s; ++t)
+                if (row[t] == b) f |= 4;
+        }
+    }
+    if (f) atomicOr(flags, f);
+    atomicAdd(&valid_count[h], (unsigned long long)nv);
+}
+
+__global__ void validate_blocks_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                                       int n_blocks, const unsigned long long* __restrict__ valid_count,
+                                       int* __restrict__ flags) {
+    const int64_t h = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    long long run = 0;
+    int f = 0;
+    for (int b = 0; b < n_blocks; ++b) {
+        int32_t c = counts[h * n_blocks + b];
+        if (c < 0) f |= 8;
+        if (offsets[h * n_blocks + b] != run) f |= 8;
+        run += c;
+    }
+    if ((unsigned long long)run != valid_count[h]) f |= 8;
+    if (f) atomicOr(flags, f);
+}
+
+__global__ void validate_flat_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                                     const int32_t* __restrict__ flat, int64_t N, int width, int B,
+                                     int n_blocks, int* __restrict__ flags) {
+    const int64_t h = blockIdx.y;
+    const int b = blockIdx.x;
+    const int32_t c = counts[h * n_blocks + b];
+    const int32_t o = offsets[h * n_blocks + b];
+    if (c < 0 || o < 0 || (int64_t)o + c > N * width) return;  // reported by the blocks check
+    const int32_t* sl = flat + h * N * width + o;
+    int f = 0;
+    for (int p = threadIdx.x; p < c; p += blockDim.x) {
+        int32_t q = sl[p];
+        if (q < (int64_t)b * B || q >= N) f |= 16;
+        if (p > 0 && sl[p - 1] >= q) f |= 16;
+    }
+    if (f) atomicOr(flags, f);
+}
+
+// varlen workspace layout: [err int | cc int32 (bh * n_chunks * n)]
+struct VarlenGeom {
+    int TQ;
+    int n_chunks;
+    int n_blocks;
+};
+
+static VarlenGeom varlen_geom(int64_t n_tokens, int block_size) {
+    VarlenGeom g;
+    g.n_blocks = (int)ceil_div(n_tokens, block_size);
+    int64_t tq = 128;
+    while (ceil_div(n_tokens, tq) * (int64_t)g.n_blocks > (4ll << 20) && tq < (1 << 20)) tq *= 2;
+    g.TQ = (int)tq;
+    g.n_chunks = (int)ceil_div(n_tokens, tq);
+    return g;
+}
+
+static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int B, int32_t* counts,
+                      int32_t* offsets, int32_t* flat, int32_t* row_pos, void* ws, size_t ws_bytes,
+                      cudaStream_t s, bool sync_range_check) {
+    VarlenGeom g = varlen_geom(N, B);
+    if (g.n_blocks > 16384) return MOBA_ERR_UNSUPPORTED;
+    size_t need = 256 + (size_t)bh * g.n_chunks * g.n_blocks * sizeof(int32_t);
+    if (ws_bytes < need) return MOBA_ERR_WORKSPACE;
+    int* err = (int*)ws;
+    int32_t* cc = (int32_t*)((char*)ws + 256);
+    StageTimer tm(T_VARLEN, s);
+    cudaMemsetAsync(err, 0, sizeof(int), s);
+    size_t hsmem = (size_t)g.n_blocks * sizeof(int);
+    if (hsmem > 48 * 1024) {
+        cudaFuncSetAttribute(varlen_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+        cudaFuncSetAttribute(varlen_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+    }
+    varlen_count_kernel<<<dim3(g.n_chunks, (unsigned)bh), 256, hsmem, s>>>(topk, N, width, g.n_blocks, g.TQ,
+                                                                        g.n_chunks, cc, err);
+    int st = check_launch("varlen_count_kernel");
+    if (st) return st;
+    if (sync_range_check) {
+        int herr = 0;
+        cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (herr) return MOBA_ERR_PLAN;
+    }
+    varlen_scan_kernel<<<(unsigned)bh, 1024, 0, s>>>(cc, g.n_blocks, g.n_chunks, counts, offsets);
+    st = check_launch("varlen_scan_kernel");
+    if (st) return st;
+    varlen_scatter_kernel<<<dim3(g.n_chunks, (unsigned)bh), 32, hsmem, s>>>(
+        topk, N, width, g.n_blocks, g.TQ, g.n_chunks, cc, offsets, flat, row_pos);
+    return check_launch("varlen_scatter_kernel");
+}
+
+template <int D, int KMAX>
+static void launch_route(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k,
+                         int32_t* topk, cudaStream_t s) {
+    dim3 grid((unsigned)ceil_div(N, kRouteQ), (unsigned)bh);
+    const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1)) * sizeof(float);
+    cudaFuncSetAttribute(route_topk_fp32_kernel<D, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    route_topk_fp32_kernel<D, KMAX><<<grid, kRouteThreads, smem, s>>>((const __nv_bfloat16*)q, cent, N, B,
+                                                                   top_k, topk);
+}
+
+template <int D>
+static int dispatch_route_k(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k,
+                            int32_t* topk, cudaStream_t s) {
+    if (top_k <= 1) launch_route<D, 1>(q, cent, bh, N, B, top_k, topk, s);
+    else if (top_k <= 2) launch_route<D, 2>(q, cent, bh, N, B, top_k, topk, s);
+    else if (top_k <= 4) launch_route<D, 4>(q, cent, bh, N, B, top_k, topk, s);
+    else if (top_k <= 8) launch_route<D, 8>(q, cent, bh, N, B, top_k, topk, s);
+    else if (top_k <= 16) launch_route<D, 16>(q, cent, bh, N, B, top_k, topk, s);
+    else if (top_k <= 32) launch_route<D, 32>(q, cent, bh, N, B, top_k, topk, s);
+    else return MOBA_ERR_UNSUPPORTED;
+    return check_launch("route_topk_fp32_kernel");
+}
+
+}  // namespace moba
+
+using namespace moba;
+
+extern "C" size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int block_size, int top_k) {
+    (void)top_k;
+    if (block_size < 1 || n_tokens < 1) return 0;
+    VarlenGeom g = varlen_geom(n_tokens, block_size);
+    return 256 + (size_t)bh * g.n_chunks * g.n_blocks * sizeof(int32_t);
+}
+
+extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int64_t n_tokens, int head_dim,
+                          int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
+                          int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1) return MOBA_ERR_SHAPE;
+    if (top_k < 1) return MOBA_ERR_CONFIG;
+    if (top_k > 31) return MOBA_ERR_UNSUPPORTED;
+    if (mode != MOBA_ROUTE_FP32 && mode != MOBA_ROUTE_TC) return MOBA_ERR_CONFIG;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st;
+    {
+    StageTimer tm(T_ROUTE, s);
+    if (head_dim == 64) st = dispatch_route_k<64>(q, centroids, bh, n_tokens, block_size, top_k, topk, s);
+    else if (head_dim == 128) st = dispatch_route_k<128>(q, centroids, bh, n_tokens, block_size, top_k, topk, s);
+    else return MOBA_ERR_UNSUPPORTED;
+    }
+    if (st) return st;
+    return run_varlen(topk, bh, n_tokens, top_k + 1, block_size, counts, offsets, flat, row_pos, workspace,
+                      workspace_bytes, s, false);
+}
+
+extern "C" int moba_varlen(const int32_t* topk, int64_t bh, int64_t n_tokens, int width, int block_size,
+                           int32_t* counts, int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+    if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
+    if (width > 32) return MOBA_ERR_UNSUPPORTED;
+    return run_varlen(topk, bh, n_tokens, width, block_size, counts, offsets, flat, row_pos, workspace,
+                      workspace_bytes, (cudaStream_t)stream, true);
+}
+
+extern "C" int moba_plan_row_pos(const int32_t* topk, const int32_t* counts, const int32_t* offsets,
+                                 const int32_t* flat, int64_t bh, int64_t n_tokens, int width, int block_size,
+                                 int32_t* row_pos, void* stream) {
+    if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
+    int n_blocks = (int)ceil_div(n_tokens, block_size);
+    dim3 grid((unsigned)ceil_div(n_tokens * width, 256), (unsigned)bh);
+    plan_row_pos_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(topk, counts, offsets, flat, n_tokens, width,
+                                                                n_blocks, row_pos);
+    return check_launch("plan_row_pos_kernel");
+}
+
+extern "C" int moba_validate_plan(const int32_t* topk, const int32_t* counts, const int32_t* offsets,
+                                  const int32_t* flat, int64_t bh, int64_t n_tokens, int width, int block_size,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+    if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
+    size_t need = 256 + (size_t)bh * sizeof(unsigned long long);
+    if (workspace_bytes < need) return MOBA_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    int n_blocks = (int)ceil_div(n_tokens, block_size);
+    int* flags = (int*)workspace;
+    unsigned long long* vc = (unsigned long long*)((char*)workspace + 256);
+    cudaMemsetAsync(workspace, 0, need, s);
+    validate_rows_kernel<<<dim3((unsigned)ceil_div(n_tokens, 256), (unsigned)bh), 256, 0, s>>>(
+        topk, n_tokens, width, block_size, n_blocks, vc, flags);
+    check_launch("validate_rows_kernel");
+    validate_blocks_kernel<<<(unsigned)bh, 32, 0, s>>>(counts, offsets, n_blocks, vc, flags);
+    int hf = 0;
+    cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    int st = check_launch("validate_plan");
+    if (st) return st;
+    if (hf) return MOBA_ERR_PLAN;
+    // slices are only inspected once counts/offsets are known consistent
+    validate_flat_kernel<<<dim3((unsigned)n_blocks, (unsigned)bh), 256, 0, s>>>(counts, offsets, flat, n_tokens,
+                                                                             width, block_size, n_blocks, flags);
+    cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    st = check_launch("validate_flat_kernel");
+    if (st) return st;
+    return hf ? MOBA_ERR_PLAN : MOBA_OK;
+}

@@ -1,0 +1,325 @@
+"""GPU parity: the CUDA path against the reference fixtures and the oracle.
+
+Runs on a B200 (`pytest -m gpu`). Every call goes through the package's
+reference-shaped API, i.e. through libmoba_b200.so's C ABI.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN, golden_names
+from helpers import assert_close, bf16_round, unexcused_routing_rows
+from oracle import moba_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2511_11571_b200 as mb  # noqa: E402
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+
+
+def f64(x):
+    return np.asarray(x, dtype=np.float64)
+
+
+def cfg_of(g):
+    return mb.MobaConfig(block_size_B=int(g["B"]), top_k=int(g["k"]), head_dim_d=int(g["d"]),
+                         conv_width=int(g["width"]))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_centroids_and_conv_vs_reference(name):
+    g = load(name)
+    B, width = int(g["B"]), int(g["width"])
+    K = f64(g["K"])
+    if width:
+        kern = mb.ConvKernel(g["W"])
+        Kc = mb.key_conv_forward(K, kern)
+        assert_close(Kc, g["Kc"], "key_conv_forward", max_abs=3e-2, rel=5e-3)
+        cents = mb.compute_centroids(K, B)  # raw-K centroids path
+        ref_c, _ = orc.centroids(K, B)
+        np.testing.assert_allclose(cents.centroids, ref_c, rtol=1e-5, atol=1e-6)
+    else:
+        cents = mb.compute_centroids(K, B)
+        np.testing.assert_allclose(cents.centroids, g["centroids"], rtol=1e-5, atol=1e-6)
+        assert np.array_equal(cents.block_lengths, g["block_lengths"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_routing_vs_reference(name):
+    g = load(name)
+    B, k, width = int(g["B"]), int(g["k"]), int(g["width"])
+    cfg = cfg_of(g)
+    Q, K = f64(g["Q"]), f64(g["K"])
+    if width:
+        # route on the fused conv path: centroids of the fp32 K' (moba_attn)
+        qt = torch.tensor(g["Q"]).cuda().bfloat16()[None]
+        kt = torch.tensor(g["K"]).cuda().bfloat16()[None]
+        w = torch.tensor(g["W"], dtype=torch.float32).cuda()
+        from paper_2511_11571_b200 import _device
+        dp = _device.padded_dim(int(g["d"]))
+        pad = lambda t: torch.nn.functional.pad(t, (0, dp - t.shape[-1]))
+        cent, _ = _device.centroids(pad(kt).contiguous(), B, pad(w).contiguous())
+        plan = _device.route(pad(qt).contiguous(), cent, B, k)
+        topk = plan.topk_indices
+        ref_cents = g["centroids"]
+    else:
+        plan = mb.build_plan(Q, K, cfg)
+        topk = plan.topk_indices
+        ref_cents = g["centroids"]
+    bad, ndiff = unexcused_routing_rows(Q, ref_cents, topk, g["topk"], B, k)
+    assert not bad, f"{len(bad)} rows differ beyond ties (of {ndiff} differing rows): {bad[:10]}"
+    if ndiff == 0:
+        assert np.array_equal(plan.counts, g["counts"])
+        assert np.array_equal(plan.offsets, g["offsets"])
+        assert np.array_equal(plan.flat_queries, g["flat"])
+    # invariants always
+    orc.validate_plan(orc.OraclePlan(topk, plan.counts, plan.offsets, plan.flat_queries), int(g["N"]), B)
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("schedule", ["deterministic", "parallel"])
+def test_attention_on_reference_plan(name, schedule):
+    """Forward + backward on the reference's own plan vs its outputs."""
+    g = load(name)
+    cfg = cfg_of(g)
+    Q, V, dO = f64(g["Q"]), f64(g["V"]), f64(g["dO"])
+    Kc = f64(g["Kc"]) if int(g["width"]) else f64(g["K"])
+    plan = mb.build_varlen(g["topk"], len(g["counts"]))
+    assert np.array_equal(plan.flat_queries, g["flat"])
+    res = mb.moba_forward(Q, Kc, V, plan, cfg)
+    assert_close(res.output, g["O"], f"{name} O")
+    assert_close(res.logsumexp, g["LSE"], f"{name} LSE")
+    dQ, dK, dV = mb.moba_backward(Q, Kc, V, res.output, dO, res.logsumexp, plan, cfg, schedule=schedule)
+    assert_close(dQ, g["dQ"], f"{name} dQ")
+    assert_close(dK, g["dK"], f"{name} dK")
+    assert_close(dV, g["dV"], f"{name} dV")
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_end_to_end_vs_oracle_on_own_plan(name):
+    """moba_attention end to end; the oracle re-runs the attention on the
+    GPU's own plan (so routing near-ties cannot masquerade as errors)."""
+    g = load(name)
+    cfg = cfg_of(g)
+    if int(g["width"]):
+        pytest.skip("conv path covered by test_moba_attn_conv_autograd")
+    Q, K, V = f64(g["Q"]), f64(g["K"]), f64(g["V"])
+    res, plan = mb.moba_attention(Q, K, V, cfg)
+    op = orc.OraclePlan(plan.topk_indices, plan.counts, plan.offsets, plan.flat_queries)
+    O, L = orc.forward(Q, K, V, op, cfg.block_size_B)
+    assert_close(res.output, O, "O")
+    assert_close(res.logsumexp, L, "LSE")
+
+
+def test_hand_tie_and_block0():
+    for name in ("hand_tie", "hand_block0"):
+        g = load(name)
+        B, k = int(g["B"]), int(g["k"])
+        d = g["Q"].shape[1]
+        cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+        idx = mb.select_topk(g["Q"], mb.compute_centroids(g["K"], B), cfg)
+        assert np.array_equal(idx, g["topk"]), name
+
+
+def test_plan_without_own_block():
+    g = load("hand_no_own_block")
+    cfg = mb.MobaConfig(block_size_B=int(g["B"]), top_k=1, head_dim_d=int(g["d"]))
+    plan = mb.build_varlen(g["topk"], 4)
+    Q, K, V, dO = (f64(g[x]) for x in ("Q", "K", "V", "dO"))
+    res = mb.moba_forward(Q, K, V, plan, cfg)
+    assert_close(res.output, g["O"], "O")
+    assert_close(res.logsumexp, g["LSE"], "LSE")
+    dQ, dK, dV = mb.moba_backward(Q, K, V, res.output, dO, res.logsumexp, plan, cfg)
+    assert_close(dQ, g["dQ"], "dQ")
+    B = int(g["B"])
+    assert not dK[B:].any() and not dV[B:].any()      # tests/test_attention.py:246-247
+    assert dK[:B].any() and dV[:B].any()
+
+
+def test_invalid_plans_rejected():
+    # tests/test_attention.py:179-193
+    rng = np.random.default_rng(11)
+    Q, K, V = (rng.standard_normal((64, 8)) for _ in range(3))
+    cfg = mb.MobaConfig(block_size_B=16, top_k=2, head_dim_d=8)
+    plan = mb.build_plan(Q, K, cfg)
+    bad_idx = plan.topk_indices.copy()
+    bad_idx[0, -1] = 3
+    bad = mb.build_varlen(bad_idx, 4)
+    with pytest.raises(mb.PlanValidationError):
+        mb.moba_forward(Q, K, V, bad, cfg)
+    broken = mb.build_plan(Q, K, cfg)
+    broken.offsets = broken.offsets + 1
+    with pytest.raises(mb.PlanValidationError):
+        mb.moba_forward(Q, K, V, broken, cfg)
+    with pytest.raises(mb.PlanValidationError):
+        mb.build_varlen(np.array([[5]]), 3)
+    with pytest.raises(mb.PlanValidationError):
+        mb.build_varlen(np.array([[-2]]), 3)
+
+
+def test_backward_zero_upstream_and_lse_checks():
+    # tests/test_attention.py:205-210, :284-292
+    rng = np.random.default_rng(12)
+    Q, K, V = (rng.standard_normal((96, 8)) for _ in range(3))
+    cfg = mb.MobaConfig(block_size_B=16, top_k=2, head_dim_d=8)
+    res, plan = mb.moba_attention(Q, K, V, cfg)
+    dQ, dK, dV = mb.moba_backward(Q, K, V, res.output, np.zeros_like(Q), res.logsumexp, plan, cfg)
+    assert not dQ.any() and not dK.any() and not dV.any()
+    with pytest.raises(mb.PlanValidationError):
+        mb.moba_backward(Q, K, V, res.output, Q, res.logsumexp[:-1], plan, cfg)
+    bad = res.logsumexp.copy()
+    bad[0] = np.inf
+    with pytest.raises(mb.PlanValidationError):
+        mb.moba_backward(Q, K, V, res.output, Q, bad, plan, cfg)
+    with pytest.raises(ValueError):
+        mb.moba_backward(Q, K, V, res.output, Q, res.logsumexp, plan, cfg, schedule="bogus")
+
+
+def test_deterministic_schedule_bitwise_repeatable():
+    # tests/test_attention.py:276-282
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    H, N, d = 4, 4096, 64
+    q, k, v, do = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(4))
+    cfg = mb.MobaConfig(block_size_B=128, top_k=8, head_dim_d=d)
+    res, plan = mb.moba_attention(q, k, v, cfg)
+    a = mb.moba_backward(q, k, v, res.output, do, res.logsumexp, plan, cfg)
+    b = mb.moba_backward(q, k, v, res.output, do, res.logsumexp, plan, cfg)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    r2, _ = mb.moba_attention(q, k, v, cfg)
+    assert torch.equal(res.output, r2.output) and torch.equal(res.logsumexp, r2.logsumexp)
+
+
+def test_dense_limit_matches_dense_attention():
+    # saturation: top_k >= n-1 -> plain causal attention (tests/test_attention.py:76-83)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    H, N, d = 2, 1024, 64
+    q, k, v = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(3))
+    cfg = mb.MobaConfig(block_size_B=128, top_k=8, head_dim_d=d)
+    res, plan = mb.moba_attention(q, k, v, cfg)
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float(), is_causal=True)
+    assert_close(res.output.float().cpu().numpy(), ref.cpu().numpy(), "dense-limit O")
+
+
+def test_c2_config_vs_oracle_sampled_heads():
+    """BASELINE configs[1] (16 heads, N=8K, d=64, B=128, k=8): routing vs the
+    f64 oracle on every head, fwd+bwd vs the oracle on the GPU plan (2 heads)."""
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    H, N, d, B, k = 16, 8192, 64, 128, 8
+    q, kk, v, do = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(4))
+    cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    res, plan = mb.moba_attention(q, kk, v, cfg)
+    dq, dk, dv = mb.moba_backward(q, kk, v, res.output, do, res.logsumexp, plan, cfg, schedule="parallel")
+    topk = plan.topk_indices
+    Qn, Kn, Vn, dOn = (t.double().cpu().numpy() for t in (q, kk, v, do))
+    total_diff = 0
+    for h in range(H):
+        c, _ = orc.centroids(Kn[h], B)
+        ref_topk = orc.select_topk(Qn[h], c, B, k)
+        bad, nd = unexcused_routing_rows(Qn[h], c, topk[h], ref_topk, B, k)
+        assert not bad, (h, bad[:5])
+        total_diff += nd
+    for h in (0, H - 1):
+        ph = plan.head(h)
+        op = orc.OraclePlan(ph.topk_indices, ph.counts, ph.offsets, ph.flat_queries)
+        O, L = orc.forward(Qn[h], Kn[h], Vn[h], op, B)
+        assert_close(res.output[h].float().cpu().numpy(), O, f"O[{h}]")
+        assert_close(res.logsumexp[h].cpu().numpy(), L, f"LSE[{h}]")
+        rQ, rK, rV = orc.backward(Qn[h], Kn[h], Vn[h], res.output[h].double().cpu().numpy(), dOn[h],
+                                  res.logsumexp[h].double().cpu().numpy(), op, B)
+        assert_close(dq[h].float().cpu().numpy(), rQ, f"dQ[{h}]")
+        assert_close(dk[h].float().cpu().numpy(), rK, f"dK[{h}]")
+        assert_close(dv[h].float().cpu().numpy(), rV, f"dV[{h}]")
+
+
+def test_moba_attn_conv_autograd():
+    """Autograd path with the key conv (config 3 shape, scaled down) vs the oracle."""
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    H, N, d, B, k, W = 2, 2048, 64, 64, 16, 3
+    q, kk, v, do = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(4))
+    w = torch.tensor(orc.random_conv_weights(W, d, seed=7), dtype=torch.float32, device="cuda")
+    q.requires_grad_(True), kk.requires_grad_(True), v.requires_grad_(True), w.requires_grad_(True)
+    out, lse = mb.moba_attn(q, kk, v, B, k, conv_weight=w, return_lse=True)
+    out.backward(do)
+    Qn, Kn, Vn, dOn = (t.detach().double().cpu().numpy() for t in (q, kk, v, do))
+    Wn = w.detach().double().cpu().numpy()
+    for h in range(H):
+        Kc = orc.key_conv_forward(Kn[h], Wn)
+        c, _ = orc.centroids(Kc, B)
+        plan_o = orc.build_plan(Qn[h], Kc, B, k)
+        O, L = orc.forward(Qn[h], Kc, Vn[h], plan_o, B)
+        # routing may differ only on ties; compare outputs where rows agree
+        assert_close(out[h].detach().float().cpu().numpy(), O, f"conv O[{h}]")
+        rQ, rKc, rV = orc.backward(Qn[h], Kc, Vn[h], O, dOn[h], L, plan_o, B)
+        rK, _ = orc.key_conv_backward(Kn[h], Wn, rKc)
+        assert_close(q.grad[h].float().cpu().numpy(), rQ, f"conv dQ[{h}]")
+        assert_close(kk.grad[h].float().cpu().numpy(), rK, f"conv dK[{h}]")
+        assert_close(v.grad[h].float().cpu().numpy(), rV, f"conv dV[{h}]")
+    # dW summed over heads
+    dW = 0
+    for h in range(H):
+        Kc = orc.key_conv_forward(Kn[h], Wn)
+        plan_o = orc.build_plan(Qn[h], Kc, B, k)
+        O, L = orc.forward(Qn[h], Kc, Vn[h], plan_o, B)
+        _, rKc, _ = orc.backward(Qn[h], Kc, Vn[h], O, dOn[h], L, plan_o, B)
+        dW = dW + orc.key_conv_backward(Kn[h], Wn, rKc)[1]
+    assert_close(w.grad.cpu().numpy(), dW, "conv dW", max_abs=5e-1, rel=1e-2)
+
+
+def test_key_conv_backward_vs_reference():
+    for name in ("conv3_n512_b64", "conv5_n300_b32"):
+        g = load(name)
+        dK, dW = mb.key_conv_backward(f64(g["K"]), mb.ConvKernel(g["W"]), f64(g["dO"]))
+        assert_close(dK, g["conv_dK"], f"{name} conv dK", max_abs=3e-2, rel=5e-3)
+        assert_close(dW, g["conv_dW"], f"{name} conv dW", max_abs=5e-2, rel=1e-2)
+
+
+@pytest.mark.slow
+def test_full_size_64k_properties():
+    """Metric-size plan (N=64K, B=128, k=8): size-independent properties —
+    conservation, prefix sums, ascending slices, causality, own block present,
+    and routing vs the f64 oracle on a sample of query rows."""
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    H, N, d, B, k = 2, 65536, 64, 128, 8
+    q, kk, v = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(3))
+    cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    res, plan = mb.moba_attention(q, kk, v, cfg)
+    assert bool(torch.isfinite(res.output.float()).all()) and bool(torch.isfinite(res.logsumexp).all())
+    E = orc.plan_entries(N, B, k)
+    counts = plan.counts_d.long()
+    assert int(counts.sum()) == H * E
+    topk = plan.topk.long()
+    i = torch.arange(N, device="cuda").view(1, N, 1)
+    assert bool(((topk <= i // B) | (topk < 0)).all())
+    assert bool((topk == (i // B)).any(dim=2).all())
+    mb.validate_plan(plan, N, cfg)
+    Qn, Kn = q.double().cpu().numpy(), kk.double().cpu().numpy()
+    rows = np.random.default_rng(0).choice(N, 2048, replace=False)
+    rows.sort()
+    for h in range(H):
+        c, _ = orc.centroids(Kn[h], B)
+        got = plan.topk_indices[h]
+        ref = got.copy()
+        ref[rows] = _select_rows(Qn[h], c, B, k, rows)   # only sampled rows can differ
+        bad, _ = unexcused_routing_rows(Qn[h], c, got, ref, B, k)
+        assert not bad, bad[:5]
+
+
+def _select_rows(Q, c, B, k, rows):
+    out = np.full((len(rows), k + 1), -1, np.int32)
+    own = rows // B
+    sel = orc._topk_rows(Q[rows] @ c.T, own, k)
+    sel[np.arange(len(rows)), own] = True
+    for r in range(len(rows)):
+        ids = np.nonzero(sel[r])[0]
+        out[r, : len(ids)] = ids
+    return out
