@@ -1,0 +1,8 @@
+# ncu evidence for the bench step: launch list + full captures of the top kernels.
+set -x
+B="python bench.py --steps 2 --warmup 3 --no-cpu --no-extra"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > /dev/null 2>&1
+for K in ${KERNELS:-moba_bwd moba_fwd route_topk}; do
+  ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 -o gpurun_out/prof_$K $B > /dev/null 2>&1
+done
+ls -la gpurun_out
