@@ -12,6 +12,8 @@
 //
 // This is the legacy-MMA (mma.sync m16n8k16) path.
 #include "common.cuh"
+#include "sm100.cuh"
+#include <cstdlib>
 
 namespace moba {
 
@@ -205,6 +207,199 @@ moba_fwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __
     }
 }
 
+
+// ---------------------------------------------------------------- tcgen05 path
+// One CTA (4 warps, one gathered query row per thread) per item at a time,
+// items in a contiguous per-CTA range so consecutive items usually share
+// (head, block) and K_j / V_j stay resident in shared memory.
+//   S[128 x BP] = Q_g K_j^T      (tcgen05.mma, fp32 in TMEM cols [0, BP))
+//   softmax rows from TMEM (tcgen05.ld), P -> smem (bf16, SW128 K-major)
+//   O[128 x D]  = P V_j          (tcgen05.mma, V as MN-major B operand)
+constexpr int kTcM = 128;
+
+template <int D>
+__global__ void __launch_bounds__(128, 1)
+moba_fwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                   const __nv_bfloat16* __restrict__ V, int64_t N, int B, int BP, int width,
+                   const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                   const int32_t* __restrict__ flat, const FwdItem* __restrict__ items,
+                   const int32_t* __restrict__ n_items_ptr, float scale_log2, uint32_t tmem_cols,
+                   __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse) {
+    using namespace sm100;
+    constexpr int SL = D / 64;  // 64-wide slabs of the head dim
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* q_s = smem;                       // [SL][128][128B]
+    uint8_t* k_s = q_s + kTcM * D * 2;         // [SL][BP][128B]
+    uint8_t* v_s = k_s + BP * D * 2;           // [SL][BP][128B]
+    uint8_t* p_s = v_s + BP * D * 2;           // [BP/64][128][128B]
+    const int pslabs = (BP + 63) / 64;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + pslabs * kTcM * 128);
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 2);
+    int32_t* qid_s = reinterpret_cast<int32_t*>(tmem_ptr + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int n_items = *n_items_ptr;
+    const int per = (n_items + gridDim.x - 1) / gridDim.x;
+    const int it0 = blockIdx.x * per;
+    const int it1 = min(n_items, it0 + per);
+
+    if (warp == 0) tmem_alloc(tmem_ptr, tmem_cols);
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_ptr;
+    const uint32_t tmem_s = tmem;           // S: columns [0, BP)
+    const uint32_t tmem_o = tmem + BP;      // O: columns [BP, BP + D)
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t idesc_s = idesc_bf16(kTcM, BP, false, false);
+    const uint32_t idesc_o = idesc_bf16(kTcM, D, false, true);
+
+    int cur_hj = -1;
+    uint32_t phase = 0;
+    for (int it = it0; it < it1; ++it) {
+        const FwdItem item = items[it];
+        const int64_t h = item.hj / n_blocks;
+        const int j = item.hj % n_blocks;
+        const int cnt = counts[item.hj];
+        const int rows = min(kTcM, cnt - item.row0);
+        const int64_t pbase = (int64_t)offsets[item.hj] + item.row0;
+        const int64_t k0 = (int64_t)j * B;
+        const int klen = (int)min64(B, N - k0);
+        const __nv_bfloat16* Qh = Q + h * N * D;
+
+        // ---- loads (all previous MMAs and TMEM reads finished: see the
+        // barrier at the end of the previous iteration)
+        const int q = (tid < rows) ? flat[h * N * width + pbase + tid] : -1;
+        qid_s[tid] = q;
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+            const uint32_t dst = smem_u32(q_s) + sw128_off(tid, c * 8, kTcM);
+            cp_async16(dst, Qh + (int64_t)max(q, 0) * D + c * 8, q >= 0);
+        }
+        if (item.hj != cur_hj) {
+            cur_hj = item.hj;
+            const __nv_bfloat16* Kh = K + (h * N + k0) * D;
+            const __nv_bfloat16* Vh = V + (h * N + k0) * D;
+            for (int e = tid; e < BP * (D / 8); e += 128) {
+                const int r = e / (D / 8), c = e % (D / 8);
+                const bool ok = r < klen;
+                const uint32_t off = sw128_off(r, c * 8, BP);
+                cp_async16(smem_u32(k_s) + off, Kh + (int64_t)(ok ? r : 0) * D + c * 8, ok);
+                cp_async16(smem_u32(v_s) + off, Vh + (int64_t)(ok ? r : 0) * D + c * 8, ok);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        __syncthreads();
+
+        // ---- S = Q K^T
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const int sl = kk >> 2, ke = (kk & 3) * 16;
+                umma_bf16(tmem_s, desc_kmajor(smem_u32(q_s) + sl * kTcM * 128, ke),
+                          desc_kmajor(smem_u32(k_s) + sl * BP * 128, ke), idesc_s, kk > 0);
+            }
+            umma_commit(&bars[0]);
+        }
+        mbar_wait(&bars[0], phase);
+        tc_fence_after();
+
+        // ---- softmax over the row (thread tid owns gathered row tid)
+        const int64_t qq = q;
+        float m = -INFINITY;
+        for (int c0 = 0; c0 < BP; c0 += 32) {
+            float sv[32];
+            tmem_ld32(tmem_s + lane_off + c0, sv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int col = c0 + i;
+                const bool ok = col < klen && k0 + col <= qq;
+                m = fmaxf(m, ok ? sv[i] * scale_log2 : -INFINITY);
+            }
+        }
+        const float mref = (m == -INFINITY) ? 0.f : m;
+        float l = 0.f;
+        for (int c0 = 0; c0 < BP; c0 += 32) {
+            float sv[32];
+            tmem_ld32(tmem_s + lane_off + c0, sv);
+            tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const int col = c0 + i;
+                const float p0 = (col < klen && k0 + col <= qq) ? fast_exp2(sv[i] * scale_log2 - mref) : 0.f;
+                const float p1 = (col + 1 < klen && k0 + col + 1 <= qq) ? fast_exp2(sv[i + 1] * scale_log2 - mref) : 0.f;
+                l += p0 + p1;
+                pk[i >> 1] = pack_bf16(p0, p1);
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const uint32_t off = sw128_off(tid, c0 + g * 8, kTcM);
+                *reinterpret_cast<uint4*>(p_s + off) = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+            }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+
+        // ---- O = P V
+        if (tid == 0) {
+            tc_fence_after();
+            for (int kk = 0; kk < BP / 16; ++kk) {
+                const int sl = kk >> 2, ke = (kk & 3) * 16;
+                umma_bf16(tmem_o, desc_kmajor(smem_u32(p_s) + sl * kTcM * 128, ke),
+                          desc_mnmajor(smem_u32(v_s), kk * 16, BP * 128), idesc_o, kk > 0);
+            }
+            umma_commit(&bars[1]);
+        }
+        mbar_wait(&bars[1], phase);
+        tc_fence_after();
+
+        // ---- epilogue: normalised partial O (bf16) and its LSE. tcgen05.ld is
+        // warp-collective: every lane loads, only rows of the tile store.
+        {
+            const float inv = 1.f / l;
+            const bool live = tid < rows;
+            __nv_bfloat16* po = part_o + (h * N * width + pbase + tid) * D;
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                float ov[32];
+                tmem_ld32(tmem_o + lane_off + c0, ov);
+                tmem_ld_wait();
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
+                if (live) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        *reinterpret_cast<uint4*>(po + c0 + g * 8) =
+                            make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+                }
+            }
+            if (live) part_lse[h * N * width + pbase + tid] = (m + __log2f(l)) * kLn2;
+        }
+        tc_fence_before();
+        __syncthreads();
+        phase ^= 1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, tmem_cols);
+    }
+}
+
 // ---------------------------------------------------------------- combine
 // One warp per query: merge its <= width partials (lse-weighted).
 template <int D>
@@ -341,27 +536,49 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     int32_t* item_off = (int32_t*)(ws + L.item_off);
     int32_t* n_items = (int32_t*)(ws + L.n_items);
     FwdItem* items = (FwdItem*)(ws + L.items);
-    fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, kFwdBM, item_off, n_items);
-    fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, kFwdBM, items);
+    const char* impl = std::getenv("MOBA_FWD_IMPL");
+    const bool use_mma = impl != nullptr && impl[0] == 'm';
+    const int bm = use_mma ? kFwdBM : kTcM;
+    fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, bm, item_off, n_items);
+    fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, bm, items);
     int st = check_launch("fwd_items", 2);
     if (st) return st;
-    const int BP = (int)ceil_div(B, 64) * 64;
-    const size_t smem = (size_t)(kFwdBM + 2 * BP) * D * 2 + kFwdBM * 4;
-    auto kern = moba_fwd_mma_kernel<D>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFwdThreads, smem);
-    if (occ < 1) return MOBA_ERR_UNSUPPORTED;
-    const int64_t max_items = bh * (ceil_div(N * width, kFwdBM) + n);
-    const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs * occ);
-    {
-    StageTimer tm(T_FWD, s);
-    kern<<<grid, kFwdThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                                         (const __nv_bfloat16*)v, N, B, BP, width, counts, offsets, flat, items,
-                                         n_items, scale * kLog2e, (__nv_bfloat16*)(ws + L.part_o),
-                                         (float*)(ws + L.part_lse));
+    const int64_t max_items = bh * (ceil_div(N * width, bm) + n);
+    if (use_mma) {
+        const int BP = (int)ceil_div(B, 64) * 64;
+        const size_t smem = (size_t)(kFwdBM + 2 * BP) * D * 2 + kFwdBM * 4;
+        auto kern = moba_fwd_mma_kernel<D>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFwdThreads, smem);
+        if (occ < 1) return MOBA_ERR_UNSUPPORTED;
+        const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs * occ);
+        StageTimer tm(T_FWD, s);
+        kern<<<grid, kFwdThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                             (const __nv_bfloat16*)v, N, B, BP, width, counts, offsets, flat, items,
+                                             n_items, scale * kLog2e, (__nv_bfloat16*)(ws + L.part_o),
+                                             (float*)(ws + L.part_lse));
+    } else {
+        const int BP = (int)ceil_div(B, 16) * 16;
+        const int pslabs = (BP + 63) / 64;
+        const size_t smem = 1024 + (size_t)kTcM * D * 2 + 2 * (size_t)BP * D * 2 + (size_t)pslabs * kTcM * 128 +
+                            64 + kTcM * 4;
+        uint32_t cols = 32;
+        while (cols < (uint32_t)(BP + D)) cols <<= 1;
+        if (cols > 512 || smem > 232448) return MOBA_ERR_UNSUPPORTED;
+        auto kern = moba_fwd_tc_kernel<D>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
+        occ = std::min<int>(occ, (int)(512 / cols));
+        if (occ < 1) return MOBA_ERR_UNSUPPORTED;
+        const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs * occ);
+        StageTimer tm(T_FWD, s);
+        kern<<<grid, 128, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, N, B,
+                                     BP, width, counts, offsets, flat, items, n_items, scale * kLog2e, cols,
+                                     (__nv_bfloat16*)(ws + L.part_o), (float*)(ws + L.part_lse));
     }
-    st = check_launch("moba_fwd_mma_kernel");
+    st = check_launch("moba_fwd_kernel");
     if (st) return st;
     StageTimer tm(T_COMBINE, s);
     const int64_t rows = bh * N;

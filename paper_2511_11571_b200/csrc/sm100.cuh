@@ -1,0 +1,134 @@
+// sm_100a building blocks: mbarriers, TMEM allocation, tcgen05.mma with
+// shared-memory descriptors, tcgen05.ld, and the proxy fences between them.
+//
+// Shared-memory operand layout used by every tensor-core kernel here
+// ("SW128 tile"): a tile of R rows x 64 bf16 (128 bytes per row) with the
+// 16-byte chunk c of row r stored at chunk (c ^ (r & 7)); tiles wider than 64
+// elements are stored as consecutive 64-wide slabs of R rows. Tile bases are
+// 1024-byte aligned. The same bytes serve as
+//   * a K-major operand (rows = M or N, 64 K-elements per slab): descriptor
+//     SBO = 1024 (8-row groups), LBO = 16, start advanced 32 B per K=16 step;
+//   * an MN-major operand (rows = K, 64 MN-elements per slab): SBO = 1024
+//     (8 K-rows), LBO = slab stride, start advanced 2048 B per K=16 step.
+#pragma once
+
+#include "common.cuh"
+
+namespace moba {
+namespace sm100 {
+
+// ---------------------------------------------------------------- mbarrier
+MOBA_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+MOBA_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+MOBA_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+MOBA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+MOBA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Blocking wait with a watchdog: a barrier that never completes (a faulted
+// async op) traps after ~10 s instead of hanging the GPU.
+MOBA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        if (clock64() - t0 > 20000000000ll) asm volatile("trap;");
+    }
+}
+
+// ---------------------------------------------------------------- fences
+// generic-proxy smem writes (st.shared / cp.async) -> async proxy (tcgen05.mma)
+MOBA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+MOBA_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+MOBA_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- TMEM
+// whole-warp calls
+MOBA_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+MOBA_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols));
+}
+
+// 32 lanes x 32 columns of fp32: thread i of the warp gets row (lane base + i),
+// columns [col, col + 32). taddr = base | (lane << 16) | col.
+MOBA_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+MOBA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- UMMA
+MOBA_DEV uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;   // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+    return d;
+}
+// K-major SW128 operand at `saddr` (rows x 64-element slab), K offset in elements
+MOBA_DEV uint64_t desc_kmajor(uint32_t slab_base, int k_elem_in_slab) {
+    return smem_desc(slab_base + k_elem_in_slab * 2, 16, 1024);
+}
+// MN-major SW128 operand: rows = K; `k_row` = first K row; slab stride = LBO
+MOBA_DEV uint64_t desc_mnmajor(uint32_t base, int k_row, uint32_t slab_stride) {
+    return smem_desc(base + k_row * 128, slab_stride, 1024);
+}
+
+// instruction descriptor, kind::f16 with bf16 inputs and fp32 accumulation
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// D[tmem] (+)= A[smem] * B[smem]; issued by one thread
+MOBA_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"((uint32_t)accumulate));
+}
+// arrive on `bar` once all previously issued tcgen05.mma of this thread complete
+MOBA_DEV void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// byte offset of element (row, col) in an SW128 tile with `rows` rows per slab
+MOBA_DEV uint32_t sw128_off(int row, int col, int rows) {
+    int slab = col >> 6;
+    int chunk = (col & 63) >> 3;
+    return slab * rows * 128 + row * 128 + ((chunk ^ (row & 7)) << 4) + (col & 7) * 2;
+}
+
+}  // namespace sm100
+}  // namespace moba
