@@ -400,6 +400,290 @@ moba_fwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     }
 }
 
+
+// ---------------------------------------------------------------- warp-specialised tcgen05 path
+// Persistent CTA, 6 warps, contiguous item range per CTA:
+//   warp 0     producer: gathers the item's 128 query rows (cp.async,
+//              completion tracked by mbarrier) and K_j / V_j when the block
+//              changes; Q and K/V double buffered
+//   warp 1     MMA issuer (one lane): S(i) = Q K^T into one of two TMEM S
+//              buffers, O(i) = P(i) V into one of two TMEM O buffers, S(i+2)
+//              issued right after O(i) so the tensor pipe always has work
+//   warps 2-5  softmax + epilogue: row r = 32*(warp%4) + lane (TMEM lane
+//              quadrant rule); softmax(i) from TMEM to bf16 P in smem, then
+//              the epilogue of item i-1 (O from TMEM -> partial in HBM)
+constexpr int kWsThreads = 192;
+
+struct FwdWsBars {
+    uint64_t q_full[2], q_empty[2], kv_full[2], kv_empty[2];
+    uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_full[2], o_empty[2];
+    uint32_t tmem;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kWsThreads, 1)
+moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                   const __nv_bfloat16* __restrict__ V, int64_t N, int B, int BP, int width,
+                   const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                   const int32_t* __restrict__ flat, const FwdItem* __restrict__ items,
+                   const int32_t* __restrict__ n_items_ptr, float scale_log2, int q_stages,
+                   __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse) {
+    using namespace sm100;
+    constexpr uint32_t kTmemCols = 512;
+    constexpr int kv_stages = 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t q_bytes = kTcM * D * 2;
+    const uint32_t kv_bytes = BP * D * 2;
+    const uint32_t p_bytes = kTcM * 128 * ((BP + 63) / 64);
+    uint8_t* q_s = smem;                                  // [q_stages][Q tile]
+    uint8_t* kv_s = q_s + q_stages * q_bytes;             // [2][K tile | V tile]
+    uint8_t* p_s = kv_s + kv_stages * 2 * kv_bytes;       // [2][P tile]
+    FwdWsBars* bars = reinterpret_cast<FwdWsBars*>(p_s + 2 * p_bytes);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int n_items = *n_items_ptr;
+    const int per = (n_items + gridDim.x - 1) / gridDim.x;
+    const int it0 = min(n_items, (int)blockIdx.x * per);
+    const int it1 = min(n_items, it0 + per);
+    const int n_local = it1 - it0;
+
+    if (warp == 1) tmem_alloc(&bars->tmem, kTmemCols);
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->q_full[s], 32);
+            mbar_init(&bars->q_empty[s], 1);
+            mbar_init(&bars->kv_full[s], 32);
+            mbar_init(&bars->kv_empty[s], 1);
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->s_empty[s], 4);
+            mbar_init(&bars->p_full[s], 4);
+            mbar_init(&bars->p_empty[s], 1);
+            mbar_init(&bars->o_full[s], 1);
+            mbar_init(&bars->o_empty[s], 4);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem;
+
+    if (n_local > 0) {
+        if (warp == 0) {
+            // ------------------------------------------------ producer
+            int prev_hj = -1, kv_uses = -1;
+            for (int li = 0; li < n_local; ++li) {
+                const FwdItem item = items[it0 + li];
+                const int64_t h = item.hj / n_blocks;
+                const int j = item.hj % n_blocks;
+                if (item.hj != prev_hj) {
+                    prev_hj = item.hj;
+                    ++kv_uses;
+                    const int ks = kv_uses % kv_stages;
+                    mbar_wait(&bars->kv_empty[ks], ((kv_uses / kv_stages) & 1) ^ 1);
+                    const int64_t k0 = (int64_t)j * B;
+                    const int klen = (int)min64(B, N - k0);
+                    const __nv_bfloat16* Kh = K + (h * N + k0) * D;
+                    const __nv_bfloat16* Vh = V + (h * N + k0) * D;
+                    const uint32_t kb = smem_u32(kv_s + ks * 2 * kv_bytes);
+                    for (int e = lane; e < BP * (D / 8); e += 32) {
+                        const int r = e / (D / 8), c = e % (D / 8);
+                        const bool ok = r < klen;
+                        const uint32_t off = sw128_off(r, c * 8, BP);
+                        cp_async16(kb + off, Kh + (int64_t)(ok ? r : 0) * D + c * 8, ok);
+                        cp_async16(kb + kv_bytes + off, Vh + (int64_t)(ok ? r : 0) * D + c * 8, ok);
+                    }
+                    cpasync_arrive_noinc(&bars->kv_full[ks]);
+                }
+                const int qs = li % q_stages;
+                mbar_wait(&bars->q_empty[qs], ((li / q_stages) & 1) ^ 1);
+                const int rows = min(kTcM, counts[item.hj] - item.row0);
+                const int32_t* fl = flat + h * N * width + offsets[item.hj] + item.row0;
+                const __nv_bfloat16* Qh = Q + h * N * D;
+                const uint32_t qb = smem_u32(q_s + qs * q_bytes);
+#pragma unroll
+                for (int rr = 0; rr < kTcM / 32; ++rr) {
+                    const int r = rr * 32 + lane;
+                    const int q = (r < rows) ? fl[r] : -1;
+                    const __nv_bfloat16* src = Qh + (int64_t)max(q, 0) * D;
+#pragma unroll
+                    for (int c = 0; c < D / 8; ++c) cp_async16(qb + sw128_off(r, c * 8, kTcM), src + c * 8, q >= 0);
+                }
+                cpasync_arrive_noinc(&bars->q_full[qs]);
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------ MMA issuer
+            const uint32_t idesc_s = idesc_bf16(kTcM, BP, false, false);
+            const uint32_t idesc_o = idesc_bf16(kTcM, D, false, true);
+            int s_hj = -1, s_kv = -1;          // kv use counter as seen by the S stream
+            int kv_of[2] = {0, 0};             // kv use index of the item in S buffer li&1
+            auto issue_s = [&](int li) {
+                const FwdItem item = items[it0 + li];
+                if (item.hj != s_hj) {
+                    s_hj = item.hj;
+                    ++s_kv;
+                    mbar_wait(&bars->kv_full[s_kv % kv_stages], (s_kv / kv_stages) & 1);
+                }
+                kv_of[li & 1] = s_kv;
+                const int qs = li % q_stages;
+                const int sb = li & 1;
+                mbar_wait(&bars->q_full[qs], (li / q_stages) & 1);
+                mbar_wait(&bars->s_empty[sb], ((li >> 1) & 1) ^ 1);
+                tc_fence_after();
+                fence_proxy_async_smem();
+                if (lane == 0) {
+                    const uint32_t qa = smem_u32(q_s + qs * q_bytes);
+                    const uint32_t ka = smem_u32(kv_s + (s_kv % kv_stages) * 2 * kv_bytes);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        umma_bf16(tmem + sb * BP, desc_kmajor(qa + sl * kTcM * 128, ke),
+                                  desc_kmajor(ka + sl * BP * 128, ke), idesc_s, kk > 0);
+                    }
+                    umma_commit(&bars->s_full[sb]);
+                    umma_commit(&bars->q_empty[qs]);
+                }
+                __syncwarp();
+            };
+            issue_s(0);
+            if (n_local > 1) issue_s(1);
+            for (int li = 0; li < n_local; ++li) {
+                const int ps = li & 1;
+                const int kvu = kv_of[ps];
+                mbar_wait(&bars->p_full[ps], (li >> 1) & 1);
+                mbar_wait(&bars->o_empty[ps], ((li >> 1) & 1) ^ 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t pa = smem_u32(p_s + ps * p_bytes);
+                    const uint32_t va = smem_u32(kv_s + (kvu % kv_stages) * 2 * kv_bytes + kv_bytes);
+                    for (int kk = 0; kk < BP / 16; ++kk) {
+                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        umma_bf16(tmem + 2 * BP + ps * D, desc_kmajor(pa + sl * kTcM * 128, ke),
+                                  desc_mnmajor(va, kk * 16, BP * 128), idesc_o, kk > 0);
+                    }
+                    umma_commit(&bars->o_full[ps]);
+                    umma_commit(&bars->p_empty[ps]);
+                    const bool last_use = (li + 1 == n_local) || items[it0 + li + 1].hj != items[it0 + li].hj;
+                    if (last_use) umma_commit(&bars->kv_empty[kvu % kv_stages]);
+                }
+                __syncwarp();
+                if (li + 2 < n_local) issue_s(li + 2);
+            }
+        } else {
+            // ------------------------------------------------ softmax + epilogue
+            const int row = 32 * (warp & 3) + lane;
+            const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+            float l_prev = 1.f, m_prev = 0.f;
+            int64_t p_prev = 0;
+            bool live_prev = false;
+            for (int li = 0; li <= n_local; ++li) {
+                float l_cur = 1.f, m_cur = 0.f;
+                int64_t p_cur = 0;
+                bool live_cur = false;
+                if (li < n_local) {
+                    const FwdItem item = items[it0 + li];
+                    const int64_t h = item.hj / n_blocks;
+                    const int j = item.hj % n_blocks;
+                    const int rows = min(kTcM, counts[item.hj] - item.row0);
+                    const int64_t pb = (int64_t)offsets[item.hj] + item.row0;
+                    live_cur = row < rows;
+                    const int64_t q = live_cur ? flat[h * N * width + pb + row] : -1;
+                    const int64_t k0 = (int64_t)j * B;
+                    const int klen = (int)min64(B, N - k0);
+                    // visible keys of this row: col < lim
+                    const int lim = (int)min64(klen, q - k0 + 1);
+                    p_cur = h * N * width + pb + row;
+                    const int sb = li & 1;
+                    mbar_wait(&bars->s_full[sb], (li >> 1) & 1);
+                    tc_fence_after();
+                    float sv[4][32];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (c * 32 < BP) tmem_ld32(tmem + sb * BP + lane_off + c * 32, sv[c]);
+                    tmem_ld_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
+                    float m = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const bool ok = c * 32 + i < lim;
+                            sv[c][i] = ok ? sv[c][i] * scale_log2 : -INFINITY;
+                            m = fmaxf(m, sv[c][i]);
+                        }
+                    const float mref = (m == -INFINITY) ? 0.f : m;
+                    float l = 0.f;
+                    mbar_wait(&bars->p_empty[sb], ((li >> 1) & 1) ^ 1);
+                    uint8_t* pt = p_s + sb * p_bytes;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (c * 32 < BP) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int i = 0; i < 32; i += 2) {
+                                const float p0 = fast_exp2(sv[c][i] - mref);
+                                const float p1 = fast_exp2(sv[c][i + 1] - mref);
+                                l += p0 + p1;
+                                pk[i >> 1] = pack_bf16(p0, p1);
+                            }
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+                                *reinterpret_cast<uint4*>(pt + sw128_off(row, c * 32 + g * 8, kTcM)) =
+                                    make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+                    l_cur = l;
+                    m_cur = m;
+                }
+                if (li >= 1) {
+                    // epilogue of item li-1
+                    const int ob = (li - 1) & 1;
+                    mbar_wait(&bars->o_full[ob], ((li - 1) >> 1) & 1);
+                    tc_fence_after();
+                    const float inv = 1.f / l_prev;
+                    __nv_bfloat16* po = part_o + p_prev * D;
+#pragma unroll
+                    for (int c0 = 0; c0 < D; c0 += 32) {
+                        float ov[32];
+                        tmem_ld32(tmem + 2 * BP + ob * D + lane_off + c0, ov);
+                        tmem_ld_wait();
+                        if (live_prev) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(ov[2 * i] * inv, ov[2 * i + 1] * inv);
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+                                *reinterpret_cast<uint4*>(po + c0 + g * 8) =
+                                    make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->o_empty[ob]);
+                    if (live_prev) part_lse[p_prev] = (m_prev + __log2f(l_prev)) * kLn2;
+                }
+                l_prev = l_cur;
+                m_prev = m_cur;
+                p_prev = p_cur;
+                live_prev = live_cur;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
 // ---------------------------------------------------------------- combine
 // One warp per query: merge its <= width partials (lse-weighted).
 template <int D>
@@ -558,6 +842,25 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
                                              (const __nv_bfloat16*)v, N, B, BP, width, counts, offsets, flat, items,
                                              n_items, scale * kLog2e, (__nv_bfloat16*)(ws + L.part_o),
                                              (float*)(ws + L.part_lse));
+    } else if (ceil_div(B, 16) * 16 <= 128 && !(impl != nullptr && impl[0] == 's')) {
+        const int BP = (int)ceil_div(B, 16) * 16;
+        const size_t q_bytes = (size_t)kTcM * D * 2, kv_bytes = (size_t)BP * D * 2;
+        const size_t p_bytes = (size_t)kTcM * 128 * ((BP + 63) / 64);
+        int q_stages = 2;
+        size_t smem = 1024 + q_stages * q_bytes + 2 * 2 * kv_bytes + 2 * p_bytes + sizeof(FwdWsBars);
+        if (smem > 232448) {
+            q_stages = 1;
+            smem = 1024 + q_bytes + 2 * 2 * kv_bytes + 2 * p_bytes + sizeof(FwdWsBars);
+        }
+        if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
+        auto kern = moba_fwd_ws_kernel<D>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs);
+        StageTimer tm(T_FWD, s);
+        kern<<<grid, kWsThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                            (const __nv_bfloat16*)v, N, B, BP, width, counts, offsets, flat, items,
+                                            n_items, scale * kLog2e, q_stages, (__nv_bfloat16*)(ws + L.part_o),
+                                            (float*)(ws + L.part_lse));
     } else {
         const int BP = (int)ceil_div(B, 16) * 16;
         const int pslabs = (BP + 63) / 64;

@@ -50,6 +50,12 @@ MOBA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// arrive on `bar` when all cp.async issued so far by this thread complete
+// (no pending-count increment: the barrier's expected count includes it)
+MOBA_DEV void cpasync_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ---------------------------------------------------------------- fences
 // generic-proxy smem writes (st.shared / cp.async) -> async proxy (tcgen05.mma)
 MOBA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
