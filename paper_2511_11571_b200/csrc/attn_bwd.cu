@@ -14,6 +14,8 @@
 //
 // This is the legacy-MMA (mma.sync m16n8k16) path.
 #include "common.cuh"
+#include "sm100.cuh"
+#include <cstdlib>
 
 namespace moba {
 
@@ -238,6 +240,333 @@ moba_bwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __
     }
 }
 
+
+// ---------------------------------------------------------------- tcgen05 path
+// Persistent CTA per (head, key block, 128-key slab) item, 6 warps:
+//   warp 0     producer: K_j / V_j once per item; per 128-query tile the
+//              gathered Q, dO rows (cp.async -> mbarrier) and L, D vectors
+//   warp 1     MMA issuer: S^T = K Q^T and dP^T = V dO^T (M = keys), then
+//              dV += P^T dO, dK += dS^T Q (TMEM accumulators across tiles)
+//              and dQ_tile = dS K (M = queries, A operand MN-major)
+//   warps 2-5  P^T = exp2(S^T - L), dS^T = P^T (dP^T - D) from TMEM into
+//              bf16 SW128 smem tiles; dQ tile TMEM -> fp32 reductions (or
+//              per-(query, block) partials); final dK, dV TMEM -> bf16
+// TMEM: S^T [0,128) dP^T [128,256) dV [256,256+D) dK [256+D,256+2D),
+//       dQ [256+2D, 256+3D) when it fits, else aliased onto S^T.
+constexpr int kBwdTcThreads = 192;
+
+struct BwdBars {
+    uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, s_empty, p_full, p_empty;
+    uint64_t dq_full, dq_empty, dkv_full, dkv_empty;
+    uint32_t tmem;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kBwdTcThreads, 1)
+moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
+                   const __nv_bfloat16* __restrict__ V, const __nv_bfloat16* __restrict__ dO,
+                   const float* __restrict__ lse, const float* __restrict__ Dd, int64_t N, int B, int width,
+                   const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                   const int32_t* __restrict__ flat, float scale, int qstages, int64_t n_items,
+                   float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
+                   __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV) {
+    using namespace sm100;
+    constexpr int KT = 128;                     // keys per item (M of the key-side MMAs)
+    constexpr int MQ = 128;                     // queries per tile
+    constexpr bool kDqAlias = (256 + 3 * D > 512);
+    constexpr uint32_t kTmemCols = 512;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr uint32_t kv_bytes = KT * D * 2;
+    constexpr uint32_t qt_bytes = MQ * D * 2;
+    constexpr uint32_t pt_bytes = KT * MQ * 2;
+    uint8_t* k_s = smem;
+    uint8_t* v_s = k_s + kv_bytes;
+    uint8_t* pt_s = v_s + kv_bytes;                  // P^T   [2 q-slabs][128 keys][128B]
+    uint8_t* dst_s = pt_s + pt_bytes;                // dS^T  same layout
+    uint8_t* stage0 = dst_s + pt_bytes;              // per stage: Q | dO | L | D | qid
+    constexpr uint32_t stage_bytes = (2 * qt_bytes + 3 * MQ * 4 + 1023) / 1024 * 1024;  // SW128 tiles need 1 KB alignment
+    BwdBars* bars = reinterpret_cast<BwdBars*>(stage0 + qstages * stage_bytes);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int slabs = (B + KT - 1) / KT;
+
+    if (warp == 1) tmem_alloc(&bars->tmem, kTmemCols);
+    if (tid == 0) {
+        mbar_init(&bars->kv_full, 32);
+        mbar_init(&bars->kv_empty, 1);
+        for (int st = 0; st < 2; ++st) {
+            mbar_init(&bars->qd_full[st], 64);
+            mbar_init(&bars->qd_empty[st], 1);
+        }
+        mbar_init(&bars->s_full, 1);
+        mbar_init(&bars->s_empty, 4);
+        mbar_init(&bars->p_full, 4);
+        mbar_init(&bars->p_empty, 1);
+        mbar_init(&bars->dq_full, 1);
+        mbar_init(&bars->dq_empty, 4);
+        mbar_init(&bars->dkv_full, 1);
+        mbar_init(&bars->dkv_empty, 4);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem;
+    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+    const uint32_t t_dq = kDqAlias ? tmem : tmem + 256 + 2 * D;
+
+    auto stage_ptr = [&](int st) { return stage0 + st * stage_bytes; };
+
+    int g = 0;        // global tile counter (same sequence in every role)
+    int kv_use = 0;   // items with >= 1 tile
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int64_t h = item / ((int64_t)n_blocks * slabs);
+        const int rem = (int)(item % ((int64_t)n_blocks * slabs));
+        const int j = rem / slabs, slab = rem % slabs;
+        const int hj = (int)(h * n_blocks + j);
+        const int cnt = counts[hj];
+        const int n_tiles = (cnt + MQ - 1) / MQ;
+        const int64_t kb0 = (int64_t)j * B + slab * KT;
+        const int klen = (int)max64(0, min64(min64(KT, (int64_t)B - slab * KT), N - kb0));
+        const int32_t* fl = flat + h * N * width + offsets[hj];
+        const int64_t pbase = h * N * width + offsets[hj];
+
+        if (warp == 0) {
+            // ------------------------------------------------ producer
+            if (n_tiles > 0) {
+                mbar_wait(&bars->kv_empty, (kv_use & 1) ^ 1);
+                const uint32_t kb = smem_u32(k_s), vb = smem_u32(v_s);
+                for (int e = lane; e < KT * (D / 8); e += 32) {
+                    const int r = e / (D / 8), c = e % (D / 8);
+                    const bool ok = r < klen;
+                    const int64_t src = (h * N + kb0 + (ok ? r : 0)) * D + c * 8;
+                    const uint32_t off = sw128_off(r, c * 8, KT);
+                    cp_async16(kb + off, K + src, ok);
+                    cp_async16(vb + off, V + src, ok);
+                }
+                cpasync_arrive_noinc(&bars->kv_full);
+            }
+            for (int t = 0; t < n_tiles; ++t, ++g) {
+                const int st = g % qstages;
+                mbar_wait(&bars->qd_empty[st], ((g / qstages) & 1) ^ 1);
+                uint8_t* sp = stage_ptr(st);
+                const uint32_t qb = smem_u32(sp), db = qb + qt_bytes;
+                float* l_st = reinterpret_cast<float*>(sp + 2 * qt_bytes);
+                float* d_st = l_st + MQ;
+                int32_t* id_st = reinterpret_cast<int32_t*>(d_st + MQ);
+                const int rows = min(MQ, cnt - t * MQ);
+#pragma unroll
+                for (int rr = 0; rr < MQ / 32; ++rr) {
+                    const int r = rr * 32 + lane;
+                    const int qi = (r < rows) ? fl[t * MQ + r] : -1;
+                    const int64_t src = (h * N + max(qi, 0)) * D;
+#pragma unroll
+                    for (int c = 0; c < D / 8; ++c) {
+                        const uint32_t off = sw128_off(r, c * 8, MQ);
+                        cp_async16(qb + off, Q + src + c * 8, qi >= 0);
+                        cp_async16(db + off, dO + src + c * 8, qi >= 0);
+                    }
+                    id_st[r] = qi;
+                    l_st[r] = (qi >= 0) ? lse[h * N + qi] * kLog2eB : 0.f;
+                    d_st[r] = (qi >= 0) ? Dd[h * N + qi] : 0.f;
+                }
+                cpasync_arrive_noinc(&bars->qd_full[st]);
+                mbar_arrive(&bars->qd_full[st]);
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------ MMA issuer
+            if (n_tiles > 0) mbar_wait(&bars->kv_full, kv_use & 1);
+            const uint32_t idesc_kq = idesc_bf16(KT, MQ, false, false);   // S^T, dP^T
+            const uint32_t idesc_kd = idesc_bf16(KT, D, false, true);     // dV, dK
+            const uint32_t idesc_qd = idesc_bf16(MQ, D, true, true);      // dQ
+            const uint32_t kb = smem_u32(k_s), vb = smem_u32(v_s);
+            const uint32_t pb = smem_u32(pt_s), sb = smem_u32(dst_s);
+            for (int t = 0; t < n_tiles; ++t, ++g) {
+                const int st = g % qstages;
+                const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
+                mbar_wait(&bars->qd_full[st], (g / qstages) & 1);
+                mbar_wait(&bars->s_empty, (g & 1) ^ 1);
+                if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
+                tc_fence_after();
+                fence_proxy_async_smem();
+                if (lane == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        umma_bf16(t_s, desc_kmajor(kb + sl * KT * 128, ke), desc_kmajor(qb + sl * MQ * 128, ke),
+                                  idesc_kq, kk > 0);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        umma_bf16(t_dp, desc_kmajor(vb + sl * KT * 128, ke), desc_kmajor(db + sl * MQ * 128, ke),
+                                  idesc_kq, kk > 0);
+                    }
+                    umma_commit(&bars->s_full);
+                }
+                __syncwarp();
+                mbar_wait(&bars->p_full, g & 1);
+                if (!kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
+                if (t == 0) mbar_wait(&bars->dkv_empty, (kv_use & 1) ^ 1);
+                tc_fence_after();
+                fence_proxy_async_smem();
+                if (lane == 0) {
+                    // dV += P^T dO ; dK += dS^T Q   (K = queries)
+#pragma unroll
+                    for (int kk = 0; kk < MQ / 16; ++kk) {
+                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        const bool acc = (t > 0) || (kk > 0);
+                        umma_bf16(t_dv, desc_kmajor(pb + sl * KT * 128, ke), desc_mnmajor(db, kk * 16, MQ * 128),
+                                  idesc_kd, acc);
+                        umma_bf16(t_dk, desc_kmajor(sb + sl * KT * 128, ke), desc_mnmajor(qb, kk * 16, MQ * 128),
+                                  idesc_kd, acc);
+                    }
+                    // dQ_tile = dS K   (M = queries from dS^T as MN-major A, K = keys)
+#pragma unroll
+                    for (int kk = 0; kk < KT / 16; ++kk) {
+                        umma_bf16(t_dq, desc_mnmajor(sb, kk * 16, KT * 128), desc_mnmajor(kb, kk * 16, KT * 128),
+                                  idesc_qd, kk > 0);
+                    }
+                    umma_commit(&bars->dq_full);
+                    umma_commit(&bars->p_empty);
+                    umma_commit(&bars->qd_empty[st]);
+                    if (t + 1 == n_tiles) {
+                        umma_commit(&bars->dkv_full);
+                        umma_commit(&bars->kv_empty);
+                    }
+                }
+                __syncwarp();
+            }
+        } else {
+            // ------------------------------------------------ softmax-bwd + epilogues
+            const int quad = warp & 3;
+            const int row = 32 * quad + lane;                     // key row (S^T/dP^T/dK/dV) or query row (dQ)
+            const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+            const int64_t key = kb0 + row;
+            for (int t = 0; t < n_tiles; ++t, ++g) {
+                const int st = g % qstages;
+                uint8_t* sp = stage_ptr(st);
+                const float* l_st = reinterpret_cast<const float*>(sp + 2 * qt_bytes);
+                const float* d_st = l_st + MQ;
+                const int32_t* id_st = reinterpret_cast<const int32_t*>(d_st + MQ);
+                mbar_wait(&bars->s_full, g & 1);
+                tc_fence_after();
+                // this row's query id for the dQ epilogue (the stage may be
+                // refilled once the dQ MMA completes)
+                const int qi = id_st[row];
+                mbar_wait(&bars->p_empty, (g & 1) ^ 1);
+                const bool krow_ok = row < klen;
+#pragma unroll 1
+                for (int c0 = 0; c0 < MQ; c0 += 32) {
+                    float sv[32], dpv[32];
+                    tmem_ld32(t_s + lane_off + c0, sv);
+                    tmem_ld32(t_dp + lane_off + c0, dpv);
+                    tmem_ld_wait();
+                    uint32_t pk[16], dk[16];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        float pv[2], dsv[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int c = c0 + i + u;
+                            const int qi = id_st[c];
+                            const bool ok = krow_ok && qi >= 0 && key <= (int64_t)qi;
+                            const float p = ok ? fast_exp2(sv[i + u] * kLog2eB * scale - l_st[c]) : 0.f;
+                            pv[u] = p;
+                            dsv[u] = p * (dpv[i + u] - d_st[c]);
+                        }
+                        pk[i >> 1] = pack_bf16(pv[0], pv[1]);
+                        dk[i >> 1] = pack_bf16(dsv[0], dsv[1]);
+                    }
+#pragma unroll
+                    for (int gq = 0; gq < 4; ++gq) {
+                        const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
+                        *reinterpret_cast<uint4*>(pt_s + off) = make_uint4(pk[4 * gq], pk[4 * gq + 1], pk[4 * gq + 2], pk[4 * gq + 3]);
+                        *reinterpret_cast<uint4*>(dst_s + off) = make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]);
+                    }
+                }
+                tc_fence_before();
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&bars->s_empty);
+                    mbar_arrive(&bars->p_full);
+                }
+                // dQ tile: TMEM lane = query row of the tile
+                mbar_wait(&bars->dq_full, g & 1);
+                tc_fence_after();
+                const int r_in = t * MQ + row;
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(t_dq + lane_off + c0, v);
+                    tmem_ld_wait();
+                    if (qi >= 0) {
+                        if (dq_part != nullptr) {
+                            float* dst = dq_part + slab * part_stride + (pbase + r_in) * D + c0;
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4)
+                                *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        } else {
+                            float* dst = dq_acc + (h * N + qi) * D + c0;
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4) red_add_f32x4(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->dq_empty);
+            }
+            // ---- dK, dV of this slab (zeros when no query attends)
+            if (n_tiles > 0) {
+                mbar_wait(&bars->dkv_full, kv_use & 1);
+                tc_fence_after();
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                float kv[32], vv[32];
+                if (n_tiles > 0) {
+                    tmem_ld32(t_dk + lane_off + c0, kv);
+                    tmem_ld32(t_dv + lane_off + c0, vv);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) kv[i] = vv[i] = 0.f;
+                }
+                if (row < klen) {
+                    uint32_t pk[16], pv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        pk[i] = pack_bf16(kv[2 * i] * scale, kv[2 * i + 1] * scale);
+                        pv[i] = pack_bf16(vv[2 * i], vv[2 * i + 1]);
+                    }
+                    const int64_t o = (h * N + key) * D + c0;
+#pragma unroll
+                    for (int gq = 0; gq < 4; ++gq) {
+                        *reinterpret_cast<uint4*>(dK + o + gq * 8) = make_uint4(pk[4 * gq], pk[4 * gq + 1], pk[4 * gq + 2], pk[4 * gq + 3]);
+                        *reinterpret_cast<uint4*>(dV + o + gq * 8) = make_uint4(pv[4 * gq], pv[4 * gq + 1], pv[4 * gq + 2], pv[4 * gq + 3]);
+                    }
+                }
+            }
+            if (n_tiles > 0) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->dkv_empty);
+            }
+        }
+        if (n_tiles > 0) ++kv_use;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
 // D = rowsum(dO * O) and dq_acc = 0; one warp per row.
 template <int D>
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* __restrict__ dO,
@@ -342,12 +671,30 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if (st) return st;
     {
     StageTimer tm(T_BWD, s);
-    if (B > 64)
-        st = launch_bwd_main<D, 128>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale, dq_acc,
-                                     dq_part, part_stride, dk, dv, s);
-    else
-        st = launch_bwd_main<D, 64>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale, dq_acc,
-                                    dq_part, part_stride, dk, dv, s);
+    const char* impl = std::getenv("MOBA_BWD_IMPL");
+    if (impl != nullptr && impl[0] == 'm') {
+        if (B > 64)
+            st = launch_bwd_main<D, 128>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
+                                         dq_acc, dq_part, part_stride, dk, dv, s);
+        else
+            st = launch_bwd_main<D, 64>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
+                                        dq_acc, dq_part, part_stride, dk, dv, s);
+    } else {
+        const int qstages = (D == 64) ? 2 : 1;
+        const size_t stage_bytes = align_up(2 * (size_t)128 * D * 2 + 3 * 128 * 4, 1024);
+        const size_t smem = 1024 + 2 * (size_t)128 * D * 2 + 2 * (size_t)128 * 128 * 2 + qstages * stage_bytes +
+                            sizeof(BwdBars);
+        if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
+        auto kern = moba_bwd_tc_kernel<D>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t n_items = bh * ceil_div(N, B) * ceil_div(B, 128);
+        const int grid = (int)std::min<int64_t>(n_items, kNumSMs);
+        kern<<<grid, kBwdTcThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                               (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, Dd, N, B,
+                                               width, counts, offsets, flat, scale, qstages, n_items, dq_acc,
+                                               dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
+        st = check_launch("moba_bwd_tc_kernel");
+    }
     }
     if (st) return st;
     StageTimer tm(T_BWD_POST, s);
