@@ -253,7 +253,16 @@ moba_bwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __
 //              per-(query, block) partials); final dK, dV TMEM -> bf16
 // TMEM: S^T [0,128) dP^T [128,256) dV [256,256+D) dK [256+D,256+2D),
 //       dQ [256+2D, 256+3D) when it fits, else aliased onto S^T.
-constexpr int kBwdTcThreads = 192;
+__device__ long long* g_trace = nullptr;
+static long long* g_last_trace = nullptr;
+#define TRACE(slot) do { if (g_trace && blockIdx.x == 0 && lane == 0 && g < 64) g_trace[(g) * 16 + (slot)] = clock64(); } while (0)
+
+constexpr int kSmWarps = 8;                               // softmax-bwd warps
+constexpr int kPrWarps = 4;                               // producer (gather) warps
+constexpr int kMmaWarp = kPrWarps;                        // MMA issuer warp index
+constexpr int kSm0 = kPrWarps + 1;                        // first softmax warp
+constexpr int kDq0 = kSm0 + kSmWarps;                     // first dQ-epilogue warp
+constexpr int kBwdTcThreads = 32 * (kDq0 + 4);
 
 struct BwdBars {
     uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, s_empty, p_full, p_empty;
@@ -263,8 +272,8 @@ struct BwdBars {
 
 template <int D>
 __global__ void __launch_bounds__(kBwdTcThreads, 1)
-moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
-                   const __nv_bfloat16* __restrict__ V, const __nv_bfloat16* __restrict__ dO,
+moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ dO,
+                   const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const float* __restrict__ lse, const float* __restrict__ Dd, int64_t N, int B, int width,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                    const int32_t* __restrict__ flat, float scale, int qstages, int64_t n_items,
@@ -284,7 +293,10 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     uint8_t* v_s = k_s + kv_bytes;
     uint8_t* pt_s = v_s + kv_bytes;                  // P^T   [2 q-slabs][128 keys][128B]
     uint8_t* dst_s = pt_s + pt_bytes;                // dS^T  same layout
-    uint8_t* stage0 = dst_s + pt_bytes;              // per stage: Q | dO | L | D | qid
+    uint8_t* stg_s = dst_s + pt_bytes;               // dQ staging: 128 rows x (D fp32 + 16 B pad)
+    constexpr bool kStage = (D == 64);               // D = 128 has no room for it
+    constexpr uint32_t kStgRow = D * 4 + 16;
+    uint8_t* stage0 = stg_s + (kStage ? (MQ * kStgRow + 1023) / 1024 * 1024 : 0);   // per stage: Q | dO | L | D | qid
     constexpr uint32_t stage_bytes = (2 * qt_bytes + 3 * MQ * 4 + 1023) / 1024 * 1024;  // SW128 tiles need 1 KB alignment
     BwdBars* bars = reinterpret_cast<BwdBars*>(stage0 + qstages * stage_bytes);
 
@@ -292,22 +304,22 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     const int n_blocks = (int)((N + B - 1) / B);
     const int slabs = (B + KT - 1) / KT;
 
-    if (warp == 1) tmem_alloc(&bars->tmem, kTmemCols);
+    if (warp == kMmaWarp) tmem_alloc(&bars->tmem, kTmemCols);
     if (tid == 0) {
-        mbar_init(&bars->kv_full, 32);
+        mbar_init(&bars->kv_full, 1);
         mbar_init(&bars->kv_empty, 1);
         for (int st = 0; st < 2; ++st) {
-            mbar_init(&bars->qd_full[st], 64);
-            mbar_init(&bars->qd_empty[st], 1);
+            mbar_init(&bars->qd_full[st], 2 * 32 * kPrWarps);   // cp.async (noinc) + plain arrivals per producer lane
+            mbar_init(&bars->qd_empty[st], 1 + 4);   // MMA commit + dQ warps (ids read)
         }
         mbar_init(&bars->s_full, 1);
-        mbar_init(&bars->s_empty, 4);
-        mbar_init(&bars->p_full, 4);
+        mbar_init(&bars->s_empty, kSmWarps);
+        mbar_init(&bars->p_full, kSmWarps);
         mbar_init(&bars->p_empty, 1);
         mbar_init(&bars->dq_full, 1);
         mbar_init(&bars->dq_empty, 4);
         mbar_init(&bars->dkv_full, 1);
-        mbar_init(&bars->dkv_empty, 4);
+        mbar_init(&bars->dkv_empty, kSmWarps);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -333,49 +345,69 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
         const int32_t* fl = flat + h * N * width + offsets[hj];
         const int64_t pbase = h * N * width + offsets[hj];
 
-        if (warp == 0) {
-            // ------------------------------------------------ producer
-            if (n_tiles > 0) {
+        if (warp < kPrWarps) {
+            // ------------------------------------------------ producers
+            if (warp == 0 && lane == 0 && item == blockIdx.x) {
+                tma_prefetch_desc(&tm_k);
+                tma_prefetch_desc(&tm_v);
+            }
+            if (n_tiles > 0 && warp == 0) {
                 mbar_wait(&bars->kv_empty, (kv_use & 1) ^ 1);
-                const uint32_t kb = smem_u32(k_s), vb = smem_u32(v_s);
-                for (int e = lane; e < KT * (D / 8); e += 32) {
-                    const int r = e / (D / 8), c = e % (D / 8);
-                    const bool ok = r < klen;
-                    const int64_t src = (h * N + kb0 + (ok ? r : 0)) * D + c * 8;
-                    const uint32_t off = sw128_off(r, c * 8, KT);
-                    cp_async16(kb + off, K + src, ok);
-                    cp_async16(vb + off, V + src, ok);
+                if (lane == 0) {
+                    mbar_expect_tx(&bars->kv_full, 2 * kv_bytes);
+                    const int row0 = (int)(h * N + kb0);
+#pragma unroll
+                    for (int sl = 0; sl < D / 64; ++sl) {
+                        tma_load_2d(smem_u32(k_s) + sl * KT * 128, &tm_k, sl * 64, row0, &bars->kv_full);
+                        tma_load_2d(smem_u32(v_s) + sl * KT * 128, &tm_v, sl * 64, row0, &bars->kv_full);
+                    }
                 }
-                cpasync_arrive_noinc(&bars->kv_full);
+                __syncwarp();
             }
             for (int t = 0; t < n_tiles; ++t, ++g) {
                 const int st = g % qstages;
-                mbar_wait(&bars->qd_empty[st], ((g / qstages) & 1) ^ 1);
-                uint8_t* sp = stage_ptr(st);
-                const uint32_t qb = smem_u32(sp), db = qb + qt_bytes;
-                float* l_st = reinterpret_cast<float*>(sp + 2 * qt_bytes);
-                float* d_st = l_st + MQ;
-                int32_t* id_st = reinterpret_cast<int32_t*>(d_st + MQ);
                 const int rows = min(MQ, cnt - t * MQ);
+                // coalesced gather: 8 lanes cover one 128-B row slab, so a
+                // warp instruction touches 4 rows (4 cache lines)
+                constexpr int CPR = D / 8;                       // 16-B chunks per row
+                const int sub = lane % 8, rsub = lane / 8;
+                // warp p gathers rows 4*(p + kPrWarps*i) + rsub
+                constexpr int NI = MQ / 4 / kPrWarps;
+                int qrow[NI];
 #pragma unroll
-                for (int rr = 0; rr < MQ / 32; ++rr) {
-                    const int r = rr * 32 + lane;
-                    const int qi = (r < rows) ? fl[t * MQ + r] : -1;
+                for (int i = 0; i < NI; ++i) {
+                    const int r = 4 * (warp + kPrWarps * i) + rsub;
+                    qrow[i] = (r < rows) ? fl[t * MQ + r] : -1;
+                }
+                mbar_wait(&bars->qd_empty[st], ((g / qstages) & 1) ^ 1);
+                if (warp == 0) TRACE(0);
+                const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
+                const uint32_t l_a = qb + 2 * qt_bytes, d_a = l_a + MQ * 4, id_a = d_a + MQ * 4;
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int r = 4 * (warp + kPrWarps * i) + rsub, qi = qrow[i];
                     const int64_t src = (h * N + max(qi, 0)) * D;
 #pragma unroll
-                    for (int c = 0; c < D / 8; ++c) {
+                    for (int c = sub; c < CPR; c += 8) {
                         const uint32_t off = sw128_off(r, c * 8, MQ);
                         cp_async16(qb + off, Q + src + c * 8, qi >= 0);
                         cp_async16(db + off, dO + src + c * 8, qi >= 0);
                     }
-                    id_st[r] = qi;
-                    l_st[r] = (qi >= 0) ? lse[h * N + qi] * kLog2eB : 0.f;
-                    d_st[r] = (qi >= 0) ? Dd[h * N + qi] : 0.f;
                 }
                 cpasync_arrive_noinc(&bars->qd_full[st]);
+                // per-row vectors: warp p, lane l writes row 32 p + l
+#pragma unroll
+                for (int u = 0; u < MQ / 32 / kPrWarps; ++u) {
+                    const int r = 32 * (warp + kPrWarps * u) + lane;
+                    const int qi = (r < rows) ? fl[t * MQ + r] : -1;
+                    sts32(id_a + r * 4, (uint32_t)qi);
+                    sts32(l_a + r * 4, __float_as_uint((qi >= 0) ? lse[h * N + qi] * kLog2eB : 0.f));
+                    sts32(d_a + r * 4, __float_as_uint((qi >= 0) ? Dd[h * N + qi] : 0.f));
+                }
                 mbar_arrive(&bars->qd_full[st]);
+                if (warp == 0) TRACE(1);
             }
-        } else if (warp == 1) {
+        } else if (warp == kMmaWarp) {
             // ------------------------------------------------ MMA issuer
             if (n_tiles > 0) mbar_wait(&bars->kv_full, kv_use & 1);
             const uint32_t idesc_kq = idesc_bf16(KT, MQ, false, false);   // S^T, dP^T
@@ -387,7 +419,9 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 const int st = g % qstages;
                 const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
                 mbar_wait(&bars->qd_full[st], (g / qstages) & 1);
+                TRACE(2);
                 mbar_wait(&bars->s_empty, (g & 1) ^ 1);
+                TRACE(3);
                 if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
                 tc_fence_after();
                 fence_proxy_async_smem();
@@ -404,11 +438,13 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                         umma_bf16(t_dp, desc_kmajor(vb + sl * KT * 128, ke), desc_kmajor(db + sl * MQ * 128, ke),
                                   idesc_kq, kk > 0);
                     }
-                    umma_commit(&bars->s_full);
                 }
+                if (lane == 0) umma_commit(&bars->s_full);
                 __syncwarp();
                 mbar_wait(&bars->p_full, g & 1);
+                TRACE(4);
                 if (!kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
+                TRACE(5);
                 if (t == 0) mbar_wait(&bars->dkv_empty, (kv_use & 1) ^ 1);
                 tc_fence_after();
                 fence_proxy_async_smem();
@@ -429,6 +465,8 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                         umma_bf16(t_dq, desc_mnmajor(sb, kk * 16, KT * 128), desc_mnmajor(kb, kk * 16, KT * 128),
                                   idesc_qd, kk > 0);
                     }
+                }
+                if (lane == 0) {
                     umma_commit(&bars->dq_full);
                     umma_commit(&bars->p_empty);
                     umma_commit(&bars->qd_empty[st]);
@@ -439,94 +477,88 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 }
                 __syncwarp();
             }
-        } else {
-            // ------------------------------------------------ softmax-bwd + epilogues
+        } else if (warp < kDq0) {
+            // ------------------------------------------------ softmax-bwd (8 warps)
+            // warp pair (w, w+4) shares TMEM lane quadrant w&3; `half` picks
+            // the query columns [64*half, 64*half+64) of S^T / dP^T
             const int quad = warp & 3;
-            const int row = 32 * quad + lane;                     // key row (S^T/dP^T/dK/dV) or query row (dQ)
+            const int half = (warp - kSm0) >> 2;
+            const int row = 32 * quad + lane;                     // key row
             const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
             const int64_t key = kb0 + row;
+            const bool krow_ok = row < klen;
+            const float sl2 = kLog2eB * scale;
+            const uint32_t pt_a = smem_u32(pt_s), ds_a = smem_u32(dst_s);
             for (int t = 0; t < n_tiles; ++t, ++g) {
                 const int st = g % qstages;
-                uint8_t* sp = stage_ptr(st);
-                const float* l_st = reinterpret_cast<const float*>(sp + 2 * qt_bytes);
-                const float* d_st = l_st + MQ;
-                const int32_t* id_st = reinterpret_cast<const int32_t*>(d_st + MQ);
+                const uint32_t l_a = smem_u32(stage_ptr(st)) + 2 * qt_bytes, d_a = l_a + MQ * 4, id_a = d_a + MQ * 4;
                 mbar_wait(&bars->s_full, g & 1);
+                if (warp == kSm0) TRACE(6);
                 tc_fence_after();
-                // this row's query id for the dQ epilogue (the stage may be
-                // refilled once the dQ MMA completes)
-                const int qi = id_st[row];
+                const int rows_t = min(MQ, cnt - t * MQ);
+                // tile-uniform: slices are ascending, so if the first query is
+                // at or past the slab's last key no element of the tile is masked
+                const bool need_mask = rows_t < MQ || klen < KT || (int64_t)lds32i(id_a) < kb0 + KT - 1;
                 mbar_wait(&bars->p_empty, (g & 1) ^ 1);
-                const bool krow_ok = row < klen;
+                if (warp == kSm0) TRACE(7);
 #pragma unroll 1
-                for (int c0 = 0; c0 < MQ; c0 += 32) {
-                    float sv[32], dpv[32];
-                    tmem_ld32(t_s + lane_off + c0, sv);
-                    tmem_ld32(t_dp + lane_off + c0, dpv);
+                for (int c = 0; c < 2; ++c) {
+                    const int c0 = half * 64 + c * 32;
+                    float sv[1][32], dpv[1][32];
+                    tmem_ld32(t_s + lane_off + c0, sv[0]);
+                    tmem_ld32(t_dp + lane_off + c0, dpv[0]);
                     tmem_ld_wait();
                     uint32_t pk[16], dk[16];
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        float pv[2], dsv[2];
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 lv = lds128f(l_a + (c0 + i) * 4);
+                        const float4 dv = lds128f(d_a + (c0 + i) * 4);
+                        const float la[4] = {lv.x, lv.y, lv.z, lv.w};
+                        const float da[4] = {dv.x, dv.y, dv.z, dv.w};
+                        float pv[4], dsv[4];
+                        if (need_mask) {
+                            const int4 iv = lds128i(id_a + (c0 + i) * 4);
+                            const int ia[4] = {iv.x, iv.y, iv.z, iv.w};
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int c = c0 + i + u;
-                            const int qi = id_st[c];
-                            const bool ok = krow_ok && qi >= 0 && key <= (int64_t)qi;
-                            const float p = ok ? fast_exp2(sv[i + u] * kLog2eB * scale - l_st[c]) : 0.f;
-                            pv[u] = p;
-                            dsv[u] = p * (dpv[i + u] - d_st[c]);
+                            for (int u = 0; u < 4; ++u) {
+                                const bool ok = krow_ok && ia[u] >= 0 && key <= (int64_t)ia[u];
+                                pv[u] = ok ? fast_exp2(fmaf(sv[0][i + u], sl2, -la[u])) : 0.f;
+                            }
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) pv[u] = fast_exp2(fmaf(sv[0][i + u], sl2, -la[u]));
                         }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) dsv[u] = pv[u] * (dpv[0][i + u] - da[u]);
                         pk[i >> 1] = pack_bf16(pv[0], pv[1]);
+                        pk[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
                         dk[i >> 1] = pack_bf16(dsv[0], dsv[1]);
+                        dk[(i >> 1) + 1] = pack_bf16(dsv[2], dsv[3]);
                     }
 #pragma unroll
                     for (int gq = 0; gq < 4; ++gq) {
                         const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
-                        *reinterpret_cast<uint4*>(pt_s + off) = make_uint4(pk[4 * gq], pk[4 * gq + 1], pk[4 * gq + 2], pk[4 * gq + 3]);
-                        *reinterpret_cast<uint4*>(dst_s + off) = make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]);
+                        sts128(pt_a + off, make_uint4(pk[4 * gq], pk[4 * gq + 1], pk[4 * gq + 2], pk[4 * gq + 3]));
+                        sts128(ds_a + off, make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]));
                     }
                 }
                 tc_fence_before();
                 fence_proxy_async_smem();
                 __syncwarp();
+                if (warp == kSm0) TRACE(8);
                 if (lane == 0) {
                     mbar_arrive(&bars->s_empty);
                     mbar_arrive(&bars->p_full);
                 }
-                // dQ tile: TMEM lane = query row of the tile
-                mbar_wait(&bars->dq_full, g & 1);
-                tc_fence_after();
-                const int r_in = t * MQ + row;
-#pragma unroll
-                for (int c0 = 0; c0 < D; c0 += 32) {
-                    float v[32];
-                    tmem_ld32(t_dq + lane_off + c0, v);
-                    tmem_ld_wait();
-                    if (qi >= 0) {
-                        if (dq_part != nullptr) {
-                            float* dst = dq_part + slab * part_stride + (pbase + r_in) * D + c0;
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4)
-                                *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                        } else {
-                            float* dst = dq_acc + (h * N + qi) * D + c0;
-#pragma unroll
-                            for (int i = 0; i < 32; i += 4) red_add_f32x4(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->dq_empty);
             }
-            // ---- dK, dV of this slab (zeros when no query attends)
+            // ---- dK, dV of this slab (zeros when no query attends); D split by half
             if (n_tiles > 0) {
                 mbar_wait(&bars->dkv_full, kv_use & 1);
                 tc_fence_after();
             }
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
+            for (int cc = 0; cc < D / 64; ++cc) {
+                const int c0 = half * (D / 2) + cc * 32;
                 float kv[32], vv[32];
                 if (n_tiles > 0) {
                     tmem_ld32(t_dk + lane_off + c0, kv);
@@ -556,12 +588,76 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->dkv_empty);
             }
+        } else {
+            // ------------------------------------------------ dQ epilogue (4 warps)
+            const int quad = warp & 3;
+            const int row = 32 * quad + lane;                     // query row of the tile
+            const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+            for (int t = 0; t < n_tiles; ++t, ++g) {
+                const int st = g % qstages;
+                const uint32_t id_a = smem_u32(stage_ptr(st)) + 2 * qt_bytes + 2 * MQ * 4;
+                mbar_wait(&bars->dq_full, g & 1);
+                if (warp == kDq0) TRACE(9);
+                tc_fence_after();
+                const int qi = lds32i(id_a + row * 4);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->qd_empty[st]);   // ids read: stage may be refilled
+                const int r_in = t * MQ + row;
+                if constexpr (!kStage) {
+                    // no room for a staging buffer: vector reductions straight from registers
+#pragma unroll
+                    for (int c0 = 0; c0 < D; c0 += 32) {
+                        float v[32];
+                        tmem_ld32(t_dq + lane_off + c0, v);
+                        tmem_ld_wait();
+                        if (qi >= 0) {
+                            if (dq_part != nullptr) {
+                                float* dst = dq_part + slab * part_stride + (pbase + r_in) * D + c0;
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4)
+                                    *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            } else {
+                                float* dst = dq_acc + (h * N + qi) * D + c0;
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4) red_add_f32x4(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            }
+                        }
+                    }
+                } else {
+                // TMEM -> padded fp32 staging row -> one bulk reduce (or store) per row
+                const uint32_t srow = smem_u32(stg_s) + row * kStgRow;
+                bulk_wait_read0();                       // previous tile's bulk ops have read the row
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(t_dq + lane_off + c0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        sts128(srow + (c0 + i) * 4, make_uint4(__float_as_uint(v[i]), __float_as_uint(v[i + 1]),
+                                                               __float_as_uint(v[i + 2]), __float_as_uint(v[i + 3])));
+                }
+                fence_proxy_async_smem();
+                if (qi >= 0) {
+                    if (dq_part != nullptr)
+                        bulk_store(dq_part + slab * part_stride + (pbase + r_in) * D, srow, D * 4);
+                    else
+                        bulk_reduce_add_f32(dq_acc + (h * N + qi) * D, srow, D * 4);
+                }
+                bulk_commit();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (warp == kDq0) TRACE(10);
+                if (lane == 0) mbar_arrive(&bars->dq_empty);
+            }
         }
         if (n_tiles > 0) ++kv_use;
     }
+    if (warp >= kDq0) bulk_wait0();
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem, kTmemCols);
     }
@@ -680,17 +776,30 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
             st = launch_bwd_main<D, 64>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
                                         dq_acc, dq_part, part_stride, dk, dv, s);
     } else {
-        const int qstages = (D == 64) ? 2 : 1;
         const size_t stage_bytes = align_up(2 * (size_t)128 * D * 2 + 3 * 128 * 4, 1024);
-        const size_t smem = 1024 + 2 * (size_t)128 * D * 2 + 2 * (size_t)128 * 128 * 2 + qstages * stage_bytes +
-                            sizeof(BwdBars);
+        const size_t stg_bytes = (D == 64) ? align_up((size_t)128 * (D * 4 + 16), 1024) : 0;
+        const size_t fixed = 1024 + 2 * (size_t)128 * D * 2 + 2 * (size_t)128 * 128 * 2 + stg_bytes + sizeof(BwdBars);
+        const int qstages = (fixed + 2 * stage_bytes <= 232448) ? 2 : 1;
+        const size_t smem = fixed + qstages * stage_bytes;
         if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
+        {
+            static long long* tr = nullptr;
+            if (std::getenv("MOBA_TRACE")) {
+                if (!tr) cudaMalloc(&tr, 64 * 16 * 8);
+                cudaMemsetAsync(tr, 0, 64 * 16 * 8, s);
+            }
+            long long* trp = std::getenv("MOBA_TRACE") ? tr : nullptr;
+            cudaMemcpyToSymbolAsync(g_trace, &trp, sizeof(trp), 0, cudaMemcpyHostToDevice, s);
+            g_last_trace = trp;
+        }
+        CUtensorMap tm_k, tm_v;
+        if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh * N), D, 128) || !make_tmap_bf16(&tm_v, v, (uint64_t)(bh * N), D, 128))
+            return MOBA_ERR_CUDA;
         auto kern = moba_bwd_tc_kernel<D>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t n_items = bh * ceil_div(N, B) * ceil_div(B, 128);
         const int grid = (int)std::min<int64_t>(n_items, kNumSMs);
-        kern<<<grid, kBwdTcThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                                               (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, Dd, N, B,
+        kern<<<grid, kBwdTcThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, N, B,
                                                width, counts, offsets, flat, scale, qstages, n_items, dq_acc,
                                                dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
         st = check_launch("moba_bwd_tc_kernel");
@@ -737,4 +846,10 @@ extern "C" int moba_bwd(const void* q, const void* k, const void* v, const void*
         return launch_bwd<128>(q, k, v, out, dout, lse, bh, n_tokens, block_size, width, counts, offsets, flat,
                                row_pos, det, softmax_scale, dq, dk, dv, ws, s);
     return MOBA_ERR_UNSUPPORTED;
+}
+
+extern "C" int moba_debug_trace(long long* host, int n) {
+    if (!moba::g_last_trace) return -1;
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpy(host, moba::g_last_trace, n * 8, cudaMemcpyDeviceToHost);
 }

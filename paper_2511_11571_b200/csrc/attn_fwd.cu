@@ -618,7 +618,7 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                     const float mref = (m == -INFINITY) ? 0.f : m;
                     float l = 0.f;
                     mbar_wait(&bars->p_empty[sb], ((li >> 1) & 1) ^ 1);
-                    uint8_t* pt = p_s + sb * p_bytes;
+                    const uint32_t pt = smem_u32(p_s) + sb * p_bytes;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         if (c * 32 < BP) {
@@ -632,8 +632,8 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                             }
 #pragma unroll
                             for (int g = 0; g < 4; ++g)
-                                *reinterpret_cast<uint4*>(pt + sw128_off(row, c * 32 + g * 8, kTcM)) =
-                                    make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+                                sts128(pt + sw128_off(row, c * 32 + g * 8, kTcM),
+                                       make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]));
                         }
                     }
                     fence_proxy_async_smem();
