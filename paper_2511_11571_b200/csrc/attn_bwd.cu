@@ -291,8 +291,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     constexpr uint32_t pt_bytes = KT * MQ * 2;
     uint8_t* k_s = smem;
     uint8_t* v_s = k_s + kv_bytes;
-    uint8_t* pt_s = v_s + kv_bytes;                  // P^T   [2 q-slabs][128 keys][128B]
-    uint8_t* dst_s = pt_s + pt_bytes;                // dS^T  same layout
+    uint8_t* dst_s = v_s + kv_bytes;                 // dS^T  [2 q-slabs][128 keys][128B] (A of dQ)
     uint8_t* stg_s = dst_s + pt_bytes;               // dQ staging: 128 rows x (D fp32 + 16 B pad)
     constexpr bool kStage = (D == 64);               // D = 128 has no room for it
     constexpr uint32_t kStgRow = D * 4 + 16;
@@ -395,10 +394,9 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                     }
                 }
                 cpasync_arrive_noinc(&bars->qd_full[st]);
-                // per-row vectors: warp p, lane l writes row 32 p + l
-#pragma unroll
-                for (int u = 0; u < MQ / 32 / kPrWarps; ++u) {
-                    const int r = 32 * (warp + kPrWarps * u) + lane;
+                // per-row vectors: warps 0..3, lane l write row 32 p + l
+                if (warp < MQ / 32) {
+                    const int r = 32 * warp + lane;
                     const int qi = (r < rows) ? fl[t * MQ + r] : -1;
                     sts32(id_a + r * 4, (uint32_t)qi);
                     sts32(l_a + r * 4, __float_as_uint((qi >= 0) ? lse[h * N + qi] * kLog2eB : 0.f));
@@ -414,13 +412,15 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
             const uint32_t idesc_kd = idesc_bf16(KT, D, false, true);     // dV, dK
             const uint32_t idesc_qd = idesc_bf16(MQ, D, true, true);      // dQ
             const uint32_t kb = smem_u32(k_s), vb = smem_u32(v_s);
-            const uint32_t pb = smem_u32(pt_s), sb = smem_u32(dst_s);
+            const uint32_t sb = smem_u32(dst_s);
             for (int t = 0; t < n_tiles; ++t, ++g) {
                 const int st = g % qstages;
                 const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
                 mbar_wait(&bars->qd_full[st], (g / qstages) & 1);
                 TRACE(2);
-                mbar_wait(&bars->s_empty, (g & 1) ^ 1);
+                // P^T / dS^T of the previous tile live in the S^T / dP^T columns
+                // until its dV / dK / dQ MMAs complete (committed to dq_full)
+                if (g > 0) mbar_wait(&bars->dq_full, (g - 1) & 1);
                 TRACE(3);
                 if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
                 tc_fence_after();
@@ -449,15 +449,13 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 tc_fence_after();
                 fence_proxy_async_smem();
                 if (lane == 0) {
-                    // dV += P^T dO ; dK += dS^T Q   (K = queries)
+                    // dV += P^T dO ; dK += dS^T Q   (K = queries; P^T, dS^T bf16 in TMEM)
 #pragma unroll
                     for (int kk = 0; kk < MQ / 16; ++kk) {
-                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        const uint32_t acol = 64 * (kk >> 2) + 8 * (kk & 3);
                         const bool acc = (t > 0) || (kk > 0);
-                        umma_bf16(t_dv, desc_kmajor(pb + sl * KT * 128, ke), desc_mnmajor(db, kk * 16, MQ * 128),
-                                  idesc_kd, acc);
-                        umma_bf16(t_dk, desc_kmajor(sb + sl * KT * 128, ke), desc_mnmajor(qb, kk * 16, MQ * 128),
-                                  idesc_kd, acc);
+                        umma_bf16_ts(t_dv, t_s + acol, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, acc);
+                        umma_bf16_ts(t_dk, t_dp + acol, desc_mnmajor(qb, kk * 16, MQ * 128), idesc_kd, acc);
                     }
                     // dQ_tile = dS K   (M = queries from dS^T as MN-major A, K = keys)
 #pragma unroll
@@ -488,7 +486,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
             const int64_t key = kb0 + row;
             const bool krow_ok = row < klen;
             const float sl2 = kLog2eB * scale;
-            const uint32_t pt_a = smem_u32(pt_s), ds_a = smem_u32(dst_s);
+            const uint32_t ds_a = smem_u32(dst_s);
             for (int t = 0; t < n_tiles; ++t, ++g) {
                 const int st = g % qstages;
                 const uint32_t l_a = smem_u32(stage_ptr(st)) + 2 * qt_bytes, d_a = l_a + MQ * 4, id_a = d_a + MQ * 4;
@@ -502,15 +500,15 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 mbar_wait(&bars->p_empty, (g & 1) ^ 1);
                 if (warp == kSm0) TRACE(7);
 #pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    const int c0 = half * 64 + c * 32;
-                    float sv[1][32], dpv[1][32];
-                    tmem_ld32(t_s + lane_off + c0, sv[0]);
-                    tmem_ld32(t_dp + lane_off + c0, dpv[0]);
+                for (int c = 0; c < 4; ++c) {
+                    const int c0 = half * 64 + c * 16;
+                    float sv[16], dpv[16];
+                    tmem_ld16(t_s + lane_off + c0, sv);
+                    tmem_ld16(t_dp + lane_off + c0, dpv);
                     tmem_ld_wait();
-                    uint32_t pk[16], dk[16];
+                    uint32_t pk[8], dk[8];
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
+                    for (int i = 0; i < 16; i += 4) {
                         const float4 lv = lds128f(l_a + (c0 + i) * 4);
                         const float4 dv = lds128f(d_a + (c0 + i) * 4);
                         const float la[4] = {lv.x, lv.y, lv.z, lv.w};
@@ -522,26 +520,30 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const bool ok = krow_ok && ia[u] >= 0 && key <= (int64_t)ia[u];
-                                pv[u] = ok ? fast_exp2(fmaf(sv[0][i + u], sl2, -la[u])) : 0.f;
+                                pv[u] = ok ? fast_exp2(fmaf(sv[i + u], sl2, -la[u])) : 0.f;
                             }
                         } else {
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) pv[u] = fast_exp2(fmaf(sv[0][i + u], sl2, -la[u]));
+                            for (int u = 0; u < 4; ++u) pv[u] = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) dsv[u] = pv[u] * (dpv[0][i + u] - da[u]);
+                        for (int u = 0; u < 4; ++u) dsv[u] = pv[u] * (dpv[i + u] - da[u]);
                         pk[i >> 1] = pack_bf16(pv[0], pv[1]);
                         pk[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
                         dk[i >> 1] = pack_bf16(dsv[0], dsv[1]);
                         dk[(i >> 1) + 1] = pack_bf16(dsv[2], dsv[3]);
                     }
+                    // P^T, dS^T (bf16 pairs) back into the S^T / dP^T columns just read
+                    // (A operands of the dV / dK MMAs); dS^T also to smem for dQ
+                    tmem_st8(t_s + lane_off + half * 64 + c * 8, pk);
+                    tmem_st8(t_dp + lane_off + half * 64 + c * 8, dk);
 #pragma unroll
-                    for (int gq = 0; gq < 4; ++gq) {
+                    for (int gq = 0; gq < 2; ++gq) {
                         const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
-                        sts128(pt_a + off, make_uint4(pk[4 * gq], pk[4 * gq + 1], pk[4 * gq + 2], pk[4 * gq + 3]));
                         sts128(ds_a + off, make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]));
                     }
                 }
+                tmem_st_wait();
                 tc_fence_before();
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -778,7 +780,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     } else {
         const size_t stage_bytes = align_up(2 * (size_t)128 * D * 2 + 3 * 128 * 4, 1024);
         const size_t stg_bytes = (D == 64) ? align_up((size_t)128 * (D * 4 + 16), 1024) : 0;
-        const size_t fixed = 1024 + 2 * (size_t)128 * D * 2 + 2 * (size_t)128 * 128 * 2 + stg_bytes + sizeof(BwdBars);
+        const size_t fixed = 1024 + 2 * (size_t)128 * D * 2 + (size_t)128 * 128 * 2 + stg_bytes + sizeof(BwdBars);
         const int qstages = (fixed + 2 * stage_bytes <= 232448) ? 2 : 1;
         const size_t smem = fixed + qstages * stage_bytes;
         if (smem > 232448) return MOBA_ERR_UNSUPPORTED;

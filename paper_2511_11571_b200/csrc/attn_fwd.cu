@@ -412,7 +412,9 @@ moba_fwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 //   warps 2-5  softmax + epilogue: row r = 32*(warp%4) + lane (TMEM lane
 //              quadrant rule); softmax(i) from TMEM to bf16 P in smem, then
 //              the epilogue of item i-1 (O from TMEM -> partial in HBM)
-constexpr int kWsThreads = 192;
+constexpr int kFwPr = 4;                    // producer (gather) warps
+constexpr int kFwMma = kFwPr;               // MMA warp
+constexpr int kWsThreads = 32 * (kFwPr + 1 + 4);
 
 struct FwdWsBars {
     uint64_t q_full[2], q_empty[2], kv_full[2], kv_empty[2];
@@ -449,12 +451,12 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     const int it1 = min(n_items, it0 + per);
     const int n_local = it1 - it0;
 
-    if (warp == 1) tmem_alloc(&bars->tmem, kTmemCols);
+    if (warp == kFwMma) tmem_alloc(&bars->tmem, kTmemCols);
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars->q_full[s], 32);
+            mbar_init(&bars->q_full[s], 32 * kFwPr);
             mbar_init(&bars->q_empty[s], 1);
-            mbar_init(&bars->kv_full[s], 32);
+            mbar_init(&bars->kv_full[s], 32 * kFwPr);
             mbar_init(&bars->kv_empty[s], 1);
             mbar_init(&bars->s_full[s], 1);
             mbar_init(&bars->s_empty[s], 4);
@@ -471,8 +473,8 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     const uint32_t tmem = bars->tmem;
 
     if (n_local > 0) {
-        if (warp == 0) {
-            // ------------------------------------------------ producer
+        if (warp < kFwPr) {
+            // ------------------------------------------------ producers (coalesced gathers)
             int prev_hj = -1, kv_uses = -1;
             for (int li = 0; li < n_local; ++li) {
                 const FwdItem item = items[it0 + li];
@@ -488,7 +490,7 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                     const __nv_bfloat16* Kh = K + (h * N + k0) * D;
                     const __nv_bfloat16* Vh = V + (h * N + k0) * D;
                     const uint32_t kb = smem_u32(kv_s + ks * 2 * kv_bytes);
-                    for (int e = lane; e < BP * (D / 8); e += 32) {
+                    for (int e = warp * 32 + lane; e < BP * (D / 8); e += 32 * kFwPr) {
                         const int r = e / (D / 8), c = e % (D / 8);
                         const bool ok = r < klen;
                         const uint32_t off = sw128_off(r, c * 8, BP);
@@ -503,17 +505,19 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 const int32_t* fl = flat + h * N * width + offsets[item.hj] + item.row0;
                 const __nv_bfloat16* Qh = Q + h * N * D;
                 const uint32_t qb = smem_u32(q_s + qs * q_bytes);
+                // 8 lanes per 128-B row segment: 4 rows per warp instruction
+                const int sub = lane & 7, rsub = lane >> 3;
 #pragma unroll
-                for (int rr = 0; rr < kTcM / 32; ++rr) {
-                    const int r = rr * 32 + lane;
+                for (int i = 0; i < kTcM / 4 / kFwPr; ++i) {
+                    const int r = 4 * (warp + kFwPr * i) + rsub;
                     const int q = (r < rows) ? fl[r] : -1;
                     const __nv_bfloat16* src = Qh + (int64_t)max(q, 0) * D;
 #pragma unroll
-                    for (int c = 0; c < D / 8; ++c) cp_async16(qb + sw128_off(r, c * 8, kTcM), src + c * 8, q >= 0);
+                    for (int c = sub; c < D / 8; c += 8) cp_async16(qb + sw128_off(r, c * 8, kTcM), src + c * 8, q >= 0);
                 }
                 cpasync_arrive_noinc(&bars->q_full[qs]);
             }
-        } else if (warp == 1) {
+        } else if (warp == kFwMma) {
             // ------------------------------------------------ MMA issuer
             const uint32_t idesc_s = idesc_bf16(kTcM, BP, false, false);
             const uint32_t idesc_o = idesc_bf16(kTcM, D, false, true);
@@ -678,7 +682,7 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kFwMma) {
         tc_fence_after();
         tmem_dealloc(tmem, kTmemCols);
     }
