@@ -412,7 +412,7 @@ moba_fwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 //   warps 2-5  softmax + epilogue: row r = 32*(warp%4) + lane (TMEM lane
 //              quadrant rule); softmax(i) from TMEM to bf16 P in smem, then
 //              the epilogue of item i-1 (O from TMEM -> partial in HBM)
-constexpr int kFwPr = 4;                    // producer (gather) warps
+constexpr int kFwPr = 2;                    // producer (gather) warps
 constexpr int kFwMma = kFwPr;               // MMA warp
 constexpr int kWsThreads = 32 * (kFwPr + 1 + 4);
 
