@@ -371,7 +371,7 @@ def extra_measurements(args, dev, mb, flush):
         def moba():
             for t in (qg, kg, vg):
                 t.grad = None
-            o = mb.moba_attn(qg, kg, vg, BLOCK, TOPK)
+            o = mb.moba_attn(qg, kg, vg, BLOCK, TOPK, mode=args.route_mode)
             o.backward(do)
 
         moba()
@@ -406,7 +406,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--route-mode", choices=["fp32", "tc"], default="fp32")
+    ap.add_argument("--route-mode", choices=["fp32", "tc"], default="tc")
     ap.add_argument("--deterministic", action="store_true", help="deterministic dQ schedule")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")

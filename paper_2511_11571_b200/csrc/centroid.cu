@@ -5,6 +5,7 @@
 // (the width-1 halo rows above the block come from L2), writes K' (bf16)
 // when the conv is on, and one fp32 centroid row.
 #include "common.cuh"
+#include <algorithm>
 
 namespace moba {
 
@@ -124,31 +125,49 @@ conv_bwd_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W
         g_s[r * D + c] = g;
     }
     __syncthreads();
-    // dK and dW partial: thread owns channel c, loops rows
-    for (int c = threadIdx.x; c < D; c += blockDim.x) {
-        float dwl[kMaxConv] = {0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int r = 0; r < kConvRows; ++r) {
-            int64_t t = t0 + r;
-            if (t >= N) break;
-            float v = __bfloat162float(dKch[t * D + c]);
-            for (int l = 0; l < width; ++l) v = fmaf(W[l * D + c], g_s[(r + l) * D + c], v);
-            dK[h * N * D + t * D + c] = __float2bfloat16(v);
-            float gt = g_s[r * D + c];
-            for (int l = 0; l < width; ++l)
-                if (t - l >= 0) dwl[l] = fmaf(gt, __bfloat162float(Kh[(t - l) * D + c]), dwl[l]);
+    // dK and dW partials: thread (row group rg, channel c) handles rows rg, rg+RG, ...
+    float* red = g_s + rows * D;  // [RG][kMaxConv][D] partial dW
+    const int RG = blockDim.x / D;
+    const int c = threadIdx.x % D, rg = threadIdx.x / D;
+    float dwl[kMaxConv] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    float wl[kMaxConv];
+    for (int l = 0; l < kMaxConv; ++l) wl[l] = (l < width) ? W[l * D + c] : 0.f;
+    for (int r = rg; r < kConvRows; r += RG) {
+        const int64_t t = t0 + r;
+        if (t >= N) break;
+        float v = __bfloat162float(dKch[t * D + c]);
+        for (int l = 0; l < width; ++l) v = fmaf(wl[l], g_s[(r + l) * D + c], v);
+        dK[h * N * D + t * D + c] = __float2bfloat16(v);
+        const float gt = g_s[r * D + c];
+        for (int l = 0; l < width; ++l)
+            if (t - l >= 0) dwl[l] = fmaf(gt, __bfloat162float(Kh[(t - l) * D + c]), dwl[l]);
+    }
+    for (int l = 0; l < width; ++l) red[(rg * kMaxConv + l) * D + c] = dwl[l];
+    __syncthreads();
+    if (rg == 0) {
+        const int64_t part = h * gridDim.x + blockIdx.x;
+        for (int l = 0; l < width; ++l) {
+            float acc = 0.f;
+            for (int gI = 0; gI < RG; ++gI) acc += red[(gI * kMaxConv + l) * D + c];
+            dw_part[(part * width + l) * D + c] = acc;
         }
-        int64_t part = h * gridDim.x + blockIdx.x;
-        for (int l = 0; l < width; ++l) dw_part[(part * width + l) * D + c] = dwl[l];
     }
 }
 
 __global__ void conv_dw_reduce_kernel(const float* __restrict__ dw_part, int64_t n_parts, int width, int D,
                                       float* __restrict__ dw) {
-    int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= width * D) return;
+    // one CTA per dW element, fixed-order strided sums + tree (deterministic)
+    __shared__ float red[256];
+    const int e = blockIdx.x;
     float s = 0.f;
-    for (int64_t p = 0; p < n_parts; ++p) s += dw_part[p * width * D + e];
-    dw[e] = s;
+    for (int64_t p = threadIdx.x; p < n_parts; p += blockDim.x) s += dw_part[p * width * D + e];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) dw[e] = red[0];
 }
 
 }  // namespace moba
@@ -186,19 +205,21 @@ extern "C" int moba_conv_bwd(const void* k, const float* conv_w, int conv_width,
     if (workspace_bytes < moba_conv_bwd_workspace_size(bh, n_tokens, head_dim, conv_width))
         return MOBA_ERR_WORKSPACE;
     dim3 grid((unsigned)ceil_div(n_tokens, kConvRows), (unsigned)bh);
-    size_t smem = (size_t)(kConvRows + conv_width - 1) * head_dim * sizeof(float);
+    const int threads = std::max(head_dim, (256 / head_dim) * head_dim);
+    size_t smem = (size_t)(kConvRows + conv_width - 1) * head_dim * sizeof(float) +
+                  (size_t)(threads / head_dim) * kMaxConv * head_dim * sizeof(float);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(conv_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     cudaStream_t s = (cudaStream_t)stream;
     StageTimer tm(T_CONV_BWD, s);
-    conv_bwd_kernel<<<grid, 256, smem, s>>>((const __nv_bfloat16*)k, conv_w, conv_width,
+    conv_bwd_kernel<<<grid, threads, smem, s>>>((const __nv_bfloat16*)k, conv_w, conv_width,
                                             (const __nv_bfloat16*)dk_conv, n_tokens, head_dim,
                                             (__nv_bfloat16*)dk, (float*)workspace);
     int st = check_launch("conv_bwd_kernel");
     if (st) return st;
     int e = conv_width * head_dim;
-    conv_dw_reduce_kernel<<<(e + 127) / 128, 128, 0, s>>>((const float*)workspace, bh * grid.x,
+    conv_dw_reduce_kernel<<<e, 256, 0, s>>>((const float*)workspace, bh * grid.x,
                                                            conv_width, head_dim, dw);
     return check_launch("conv_dw_reduce_kernel");
 }

@@ -11,6 +11,7 @@
 // bf16 queries and fp32 centroids, summed in d order), and each thread keeps
 // its query's running top-k list in registers.
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace moba {
 
@@ -39,6 +40,35 @@ MOBA_DEV void topk_insert(float (&ts)[KMAX], int (&ti)[KMAX], float s, int j) {
     }
 }
 
+
+// Chunked, warp-friendly selection: each lane first compacts the candidates
+// of a 32-wide chunk that beat its (stale) threshold into a private smem
+// list with predicated stores, then the warp inserts them in lockstep. The
+// insert loop runs max-over-lanes(passes) times instead of once for every
+// candidate any lane accepts. Candidates stay in ascending block order, so
+// the (score desc, index asc) order of topk_insert is preserved.
+template <int KMAX>
+MOBA_DEV void select_chunk32(const float (&sv)[32], int j0, int lim, float (&ts)[KMAX], int (&ti)[KMAX],
+                             float* buf_s, int* buf_i) {
+    const float thr = ts[KMAX - 1];
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        if (i < lim && sv[i] > thr) {
+            buf_s[cnt * 33] = sv[i];
+            buf_i[cnt * 33] = j0 + i;
+            ++cnt;
+        }
+    }
+    const int iters = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+    for (int t = 0; t < iters; ++t) {
+        if (t < cnt) {
+            const float sc = buf_s[t * 33];
+            if (sc > ts[KMAX - 1]) topk_insert<KMAX>(ts, ti, sc, buf_i[t * 33]);
+        }
+    }
+}
+
 template <int D, int KMAX>
 __global__ void __launch_bounds__(kRouteThreads)
 route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, int64_t N,
@@ -47,6 +77,8 @@ route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restr
     float (*q_s)[kRouteQ] = reinterpret_cast<float (*)[kRouteQ]>(route_smem);
     float (*c_s)[kRouteC] = reinterpret_cast<float (*)[kRouteC]>(route_smem + D * kRouteQ);
     float (*s_s)[kRouteC + 1] = reinterpret_cast<float (*)[kRouteC + 1]>(route_smem + D * (kRouteQ + kRouteC));
+    float* sel_s = route_smem + D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1);   // [4 warps][33][33]
+    int* sel_i = reinterpret_cast<int*>(sel_s + 4 * 33 * 33);
 
     const int tid = threadIdx.x;
     const int64_t h = blockIdx.y;
@@ -124,12 +156,13 @@ route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restr
         __syncthreads();
         // selection: thread tid owns query r0 + tid; only strictly-past
         // blocks j < own compete (src/router.py:92)
-        int lim = min(kRouteC, my_own - c0);
-        if (my_i < N) {
-            for (int c = 0; c < lim; ++c) {
-                float s = s_s[tid][c];
-                if (s > ts[KMAX - 1]) topk_insert<KMAX>(ts, ti, s, c0 + c);
-            }
+        const int lim = (my_i < N) ? min(kRouteC, my_own - c0) : 0;
+        {
+            float sv[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) sv[c] = s_s[tid][c];
+            select_chunk32<KMAX>(sv, c0, lim, ts, ti, sel_s + (tid & 31) + (tid >> 5) * 33 * 33,
+                                 sel_i + (tid & 31) + (tid >> 5) * 33 * 33);
         }
     }
 
@@ -158,6 +191,168 @@ route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restr
     }
     row[nvalid] = my_own;
     for (int s = nvalid + 1; s < width; ++s) row[s] = -1;
+}
+
+
+// ---------------------------------------------------------------- tensor-core routing
+// Perf mode (MOBA_ROUTE_TC). The fp32 centroid is split into three bf16 terms
+// c = c1 + c2 + c3 (24 mantissa bits); queries are bf16 already, so every
+// product q*ci is exact in fp32 and S = Q C1^T + Q C2^T + Q C3^T accumulates
+// in fp32 on tcgen05 (TMEM). Scores agree with the FFMA path to fp32 rounding
+// (ties within ~1e-6 may resolve differently, as documented).
+__global__ void centroid_split_kernel(const float* __restrict__ cent, int64_t total, __nv_bfloat16* __restrict__ split) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const float c = cent[e];
+    const __nv_bfloat16 c1 = __float2bfloat16(c);
+    const float r1 = c - __bfloat162float(c1);
+    const __nv_bfloat16 c2 = __float2bfloat16(r1);
+    const __nv_bfloat16 c3 = __float2bfloat16(r1 - __bfloat162float(c2));
+    split[e] = c1;
+    split[total + e] = c2;
+    split[2 * total + e] = c3;
+}
+
+constexpr int kRtM = 128;   // queries per CTA (TMEM lanes)
+constexpr int kRtN = 64;    // centroids per chunk (MMA N)
+
+template <int D, int KMAX>
+__global__ void __launch_bounds__(128)
+route_topk_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
+                     int B, int top_k, int64_t split_rows, int32_t* __restrict__ topk) {
+    using namespace sm100;
+    constexpr int SL = D / 64;
+    constexpr uint32_t q_bytes = kRtM * D * 2;
+    constexpr uint32_t c_bytes = kRtN * D * 2;            // one split term of a chunk
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* q_s = smem;
+    uint8_t* c_s = q_s + q_bytes;                         // [2 buffers][3 terms][SL][128][128B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(c_s + 2 * 3 * c_bytes);   // tma[2], mma[2]
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 4);
+    float* sel_s = reinterpret_cast<float*>(tmem_ptr + 4);                   // [4 warps][33][33]
+    int* sel_i = reinterpret_cast<int*>(sel_s + 4 * 33 * 33);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t h = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * kRtM;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int width = top_k + 1;
+    const int64_t last_i = min64(r0 + kRtM, N) - 1;
+    const int max_own = (int)(last_i / B);
+    const int n_chunks = (max_own + kRtN - 1) / kRtN;
+
+    if (warp == 0) tmem_alloc(tmem_ptr, 2 * kRtN);
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_ptr;
+    const uint32_t idesc = idesc_bf16(kRtM, kRtN, false, false);
+
+    auto load_chunk = [&](int c, int buf) {   // thread 0
+        mbar_expect_tx(&bars[buf], 3 * c_bytes + (c == 0 ? q_bytes : 0));
+        if (c == 0) {
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+                tma_load_2d(smem_u32(q_s) + sl * kRtM * 128, &tm_q, sl * 64, (int)(h * N + r0), &bars[buf]);
+        }
+        const uint32_t cb = smem_u32(c_s) + buf * 3 * c_bytes;
+#pragma unroll
+        for (int term = 0; term < 3; ++term)
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+                tma_load_2d(cb + term * c_bytes + sl * kRtN * 128, &tm_c, sl * 64,
+                            (int)(term * split_rows + h * n_blocks + (int64_t)c * kRtN), &bars[buf]);
+    };
+    auto issue_mma = [&](int c) {             // thread 0
+        const int buf = c & 1;
+        mbar_wait(&bars[buf], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(q_s), cb = smem_u32(c_s) + buf * 3 * c_bytes;
+        bool acc = false;
+#pragma unroll
+        for (int term = 0; term < 3; ++term)
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const int sl = kk >> 2, ke = (kk & 3) * 16;
+                umma_bf16(tmem + buf * kRtN, desc_kmajor(qa + sl * kRtM * 128, ke),
+                          desc_kmajor(cb + term * c_bytes + sl * kRtN * 128, ke), idesc, acc);
+                acc = true;
+            }
+        umma_commit(&bars[2 + buf]);
+    };
+
+    if (tid == 0 && n_chunks > 0) {
+        load_chunk(0, 0);
+        if (n_chunks > 1) load_chunk(1, 1);
+        issue_mma(0);
+    }
+
+    const int64_t my_i = r0 + tid;
+    const int my_own = (int)(min64(my_i, N - 1) / B);
+    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+    float ts[KMAX];
+    int ti[KMAX];
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        ts[u] = -INFINITY;
+        ti[u] = 0x7fffffff;
+    }
+    for (int c = 0; c < n_chunks; ++c) {
+        const int buf = c & 1;
+        mbar_wait(&bars[2 + buf], (c >> 1) & 1);        // S(c) in TMEM, smem buffer free
+        tc_fence_after();
+        if (tid == 0) {
+            if (c + 1 < n_chunks) issue_mma(c + 1);
+            if (c + 2 < n_chunks) load_chunk(c + 2, buf);
+        }
+        const int c0 = c * kRtN;
+        const int lim = min(kRtN, my_own - c0);          // strictly-past blocks only
+        const int lane = tid & 31;
+#pragma unroll 1
+        for (int k0 = 0; k0 < kRtN; k0 += 32) {
+            if (__all_sync(0xffffffffu, k0 >= lim)) break;       // rest of the chunk is not past for this warp
+            float sv[32];
+            tmem_ld32(tmem + buf * kRtN + lane_off + k0, sv);
+            tmem_ld_wait();
+            select_chunk32<KMAX>(sv, c0 + k0, (my_i < N) ? lim - k0 : 0, ts, ti, sel_s + lane + warp * 33 * 33,
+                                 sel_i + lane + warp * 33 * 33);
+        }
+        tc_fence_before();
+        __syncthreads();                                 // S buffer may be overwritten by MMA(c + 2)
+    }
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 2 * kRtN);
+    }
+    if (my_i >= N) return;
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u)
+        if (u >= top_k) ti[u] = 0x7fffffff;
+#pragma unroll
+    for (int p = 0; p < KMAX; ++p) {
+#pragma unroll
+        for (int u = (p & 1); u + 1 < KMAX; u += 2) {
+            int a = ti[u], b = ti[u + 1];
+            ti[u] = min(a, b);
+            ti[u + 1] = max(a, b);
+        }
+    }
+    int32_t* row = topk + (h * N + my_i) * width;
+    int nvalid = 0;
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        if (ti[u] != 0x7fffffff) {
+            row[u] = ti[u];
+            ++nvalid;
+        }
+    }
+    row[nvalid] = my_own;
+    for (int s2 = nvalid + 1; s2 < width; ++s2) row[s2] = -1;
 }
 
 // ---------------------------------------------------------------- varlen
@@ -442,37 +637,59 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
 }
 
 template <int D, int KMAX>
-static void launch_route(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k,
-                         int32_t* topk, cudaStream_t s) {
+static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k, int mode,
+                        int32_t* topk, void* split_ws, cudaStream_t s) {
     dim3 grid((unsigned)ceil_div(N, kRouteQ), (unsigned)bh);
-    const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1)) * sizeof(float);
+    if (mode == MOBA_ROUTE_TC) {
+        const int64_t n = ceil_div(N, B);
+        const int64_t total = bh * n * D;
+        __nv_bfloat16* split = (__nv_bfloat16*)split_ws;
+        centroid_split_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(cent, total, split);
+        int st = check_launch("centroid_split_kernel");
+        if (st) return st;
+        CUtensorMap tm_q, tm_c;
+        if (!make_tmap_bf16(&tm_q, q, (uint64_t)(bh * N), D, kRtM) ||
+            !make_tmap_bf16(&tm_c, split, (uint64_t)(3 * bh * n), D, kRtN))
+            return MOBA_ERR_CUDA;
+        const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 4 * 33 * 33 * 4;
+        auto kern = route_topk_tc_kernel<D, KMAX>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh * n, topk);
+        return check_launch("route_topk_tc_kernel");
+    }
+    const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
     cudaFuncSetAttribute(route_topk_fp32_kernel<D, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     route_topk_fp32_kernel<D, KMAX><<<grid, kRouteThreads, smem, s>>>((const __nv_bfloat16*)q, cent, N, B,
-                                                                   top_k, topk);
+                                                                       top_k, topk);
+    return check_launch("route_topk_fp32_kernel");
 }
 
 template <int D>
-static int dispatch_route_k(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k,
-                            int32_t* topk, cudaStream_t s) {
-    if (top_k <= 1) launch_route<D, 1>(q, cent, bh, N, B, top_k, topk, s);
-    else if (top_k <= 2) launch_route<D, 2>(q, cent, bh, N, B, top_k, topk, s);
-    else if (top_k <= 4) launch_route<D, 4>(q, cent, bh, N, B, top_k, topk, s);
-    else if (top_k <= 8) launch_route<D, 8>(q, cent, bh, N, B, top_k, topk, s);
-    else if (top_k <= 16) launch_route<D, 16>(q, cent, bh, N, B, top_k, topk, s);
-    else if (top_k <= 32) launch_route<D, 32>(q, cent, bh, N, B, top_k, topk, s);
-    else return MOBA_ERR_UNSUPPORTED;
-    return check_launch("route_topk_fp32_kernel");
+static int dispatch_route_k(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k, int mode,
+                            int32_t* topk, void* split_ws, cudaStream_t s) {
+    if (top_k <= 1) return launch_route<D, 1>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+    if (top_k <= 2) return launch_route<D, 2>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+    if (top_k <= 4) return launch_route<D, 4>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+    if (top_k <= 8) return launch_route<D, 8>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+    if (top_k <= 16) return launch_route<D, 16>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+    if (top_k <= 32) return launch_route<D, 32>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+    return MOBA_ERR_UNSUPPORTED;
 }
 
 }  // namespace moba
 
 using namespace moba;
 
+// workspace: [varlen: err | chunk counts] [route tc: bf16 centroid split 3 x bh x n x 128]
+static size_t varlen_ws_bytes(int64_t bh, int64_t n_tokens, int block_size) {
+    VarlenGeom g = varlen_geom(n_tokens, block_size);
+    return align_up(256 + (size_t)bh * g.n_chunks * g.n_blocks * sizeof(int32_t), 1024);
+}
+
 extern "C" size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int block_size, int top_k) {
     (void)top_k;
     if (block_size < 1 || n_tokens < 1) return 0;
-    VarlenGeom g = varlen_geom(n_tokens, block_size);
-    return 256 + (size_t)bh * g.n_chunks * g.n_blocks * sizeof(int32_t);
+    return varlen_ws_bytes(bh, n_tokens, block_size) + 3 * (size_t)bh * ceil_div(n_tokens, block_size) * 128 * 2;
 }
 
 extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int64_t n_tokens, int head_dim,
@@ -487,8 +704,10 @@ extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int
     int st;
     {
     StageTimer tm(T_ROUTE, s);
-    if (head_dim == 64) st = dispatch_route_k<64>(q, centroids, bh, n_tokens, block_size, top_k, topk, s);
-    else if (head_dim == 128) st = dispatch_route_k<128>(q, centroids, bh, n_tokens, block_size, top_k, topk, s);
+    if (workspace_bytes < moba_route_workspace_size(bh, n_tokens, block_size, top_k)) return MOBA_ERR_WORKSPACE;
+    void* split_ws = (char*)workspace + varlen_ws_bytes(bh, n_tokens, block_size);
+    if (head_dim == 64) st = dispatch_route_k<64>(q, centroids, bh, n_tokens, block_size, top_k, mode, topk, split_ws, s);
+    else if (head_dim == 128) st = dispatch_route_k<128>(q, centroids, bh, n_tokens, block_size, top_k, mode, topk, split_ws, s);
     else return MOBA_ERR_UNSUPPORTED;
     }
     if (st) return st;

@@ -323,3 +323,39 @@ def _select_rows(Q, c, B, k, rows):
         ids = np.nonzero(sel[r])[0]
         out[r, : len(ids)] = ids
     return out
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_routing_tensor_core_mode_vs_reference(name):
+    """Perf routing mode (bf16x3 centroid split on tcgen05): same selections as
+    the reference up to score near-ties (tolerance 1e-5 on the f64 score gap)."""
+    g = load(name)
+    if int(g["d"]) > 128:
+        pytest.skip("d > 128")
+    B, k, width = int(g["B"]), int(g["k"]), int(g["width"])
+    from paper_2511_11571_b200 import _device
+    dp = _device.padded_dim(int(g["d"]))
+    pad = lambda t: torch.nn.functional.pad(t, (0, dp - t.shape[-1])).contiguous()
+    qt = pad(torch.tensor(g["Q"]).cuda().bfloat16()[None])
+    kt = pad(torch.tensor(g["K"]).cuda().bfloat16()[None])
+    w = pad(torch.tensor(g["W"], dtype=torch.float32).cuda()) if width else None
+    cent, _ = _device.centroids(kt, B, w)
+    plan = _device.route(qt, cent, B, k, mode=1)
+    bad, ndiff = unexcused_routing_rows(f64(g["Q"]), g["centroids"], plan.topk_indices, g["topk"], B, k, tol=1e-5)
+    assert not bad, f"{len(bad)} rows differ beyond ties (of {ndiff}): {bad[:10]}"
+    orc.validate_plan(orc.OraclePlan(plan.topk_indices, plan.counts, plan.offsets, plan.flat_queries),
+                      int(g["N"]), B)
+
+
+def test_routing_tensor_core_mode_c2_scale():
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    H, N, d, B, k = 4, 8192, 64, 128, 8
+    q, kk = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    p_tc = mb.build_plan(q, kk, cfg, mode="tc")
+    p_fp = mb.build_plan(q, kk, cfg, mode="fp32")
+    Qn, Kn = q.double().cpu().numpy(), kk.double().cpu().numpy()
+    for h in range(H):
+        c, _ = orc.centroids(Kn[h], B)
+        bad, nd = unexcused_routing_rows(Qn[h], c, p_tc.topk_indices[h], p_fp.topk_indices[h], B, k, tol=1e-5)
+        assert not bad, (h, bad[:5], nd)
