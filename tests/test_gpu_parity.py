@@ -359,3 +359,22 @@ def test_routing_tensor_core_mode_c2_scale():
         c, _ = orc.centroids(Kn[h], B)
         bad, nd = unexcused_routing_rows(Qn[h], c, p_tc.topk_indices[h], p_fp.topk_indices[h], B, k, tol=1e-5)
         assert not bad, (h, bad[:5], nd)
+
+
+@pytest.mark.parametrize("n_chunks", [1, 3])
+def test_host_pipeline_matches_device_path(n_chunks):
+    """moba_fwd_bwd_host (pinned host buffers, chunked over heads, copies on
+    their own streams) returns bitwise the device path's results."""
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    H, N, d, B, k = 5, 2048, 64, 128, 8
+    q, kk, v, do = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(4))
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
+    out, lse = mb.moba_attn(qg, kg, vg, B, k, mode="tc", deterministic=True, return_lse=True)
+    out.backward(do)
+    host = [t.cpu().pin_memory() for t in (q, kk, v, do)]
+    o_h, lse_h, dq_h, dk_h, dv_h = mb.moba_fwd_bwd_host(*host, B, k, n_chunks=n_chunks, mode="tc",
+                                                        deterministic=True)
+    for got, ref, nm in ((o_h, out, "O"), (lse_h, lse, "LSE"), (dq_h, qg.grad, "dQ"), (dk_h, kg.grad, "dK"),
+                         (dv_h, vg.grad, "dV")):
+        assert not got.is_cuda
+        assert torch.equal(got, ref.detach().cpu()), nm
