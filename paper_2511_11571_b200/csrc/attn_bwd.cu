@@ -723,11 +723,16 @@ __global__ void bwd_dq_combine_kernel(const float* __restrict__ dq_part, int64_t
         *reinterpret_cast<uint32_t*>(dst + c) = pack_bf16(acc[c] * scale, acc[c + 1] * scale);
 }
 
-// workspace: Dd f32 [bh*N] | dq_acc f32 [bh*N*D] | (deterministic) dq_part
-// f32 [slabs][bh*N*width*D]
+int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* Dd,
+                    int64_t bh, int64_t N, int B, int width, const int32_t* counts, const int32_t* offsets,
+                    const int32_t* flat, float scale, int* sched, float* dq_acc, float* dq_part,
+                    int64_t part_stride, void* dk, void* dv, cudaStream_t s);
+
+// workspace: sched int (256 B) | Dd f32 [bh*N] | dq_acc f32 [bh*N*D] |
+// (deterministic) dq_part f32 [slabs][bh*N*width*D]
 static int bwd_kt(int B) { return B > 64 ? 128 : 64; }
 static size_t bwd_ws(int64_t bh, int64_t N, int D, int B, int width, bool det) {
-    size_t w = align_up((size_t)bh * N * 4, 256) + align_up((size_t)bh * N * D * 4, 256);
+    size_t w = 256 + align_up((size_t)bh * N * 4, 256) + align_up((size_t)bh * N * D * 4, 256);
     if (det) w += (size_t)ceil_div(B, bwd_kt(B)) * bh * N * width * D * 4;
     return w;
 }
@@ -754,6 +759,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                       const float* lse, int64_t bh, int64_t N, int B, int width, const int32_t* counts,
                       const int32_t* offsets, const int32_t* flat, const int32_t* row_pos, bool det, float scale,
                       void* dq, void* dk, void* dv, uint8_t* ws, cudaStream_t s) {
+    int* sched = (int*)ws;
+    ws += 256;
     float* Dd = (float*)ws;
     float* dq_acc = (float*)(ws + align_up((size_t)bh * N * 4, 256));
     float* dq_part = det ? (float*)((uint8_t*)dq_acc + align_up((size_t)bh * N * D * 4, 256)) : nullptr;
@@ -770,7 +777,13 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     {
     StageTimer tm(T_BWD, s);
     const char* impl = std::getenv("MOBA_BWD_IMPL");
-    if (impl != nullptr && impl[0] == 'm') {
+    const int slabs_tc = (int)ceil_div(B, 128);
+    if (D == 64 && !(impl != nullptr && (impl[0] == 'm' || impl[0] == 't'))) {
+        // pipelined tcgen05 kernel (attn_bwd_pipe.cu); dq_part slabs follow its 128-key slabs
+        (void)slabs_tc;
+        st = launch_bwd_pipe(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale, sched, dq_acc,
+                             dq_part, part_stride, dk, dv, s);
+    } else if (impl != nullptr && impl[0] == 'm') {
         if (B > 64)
             st = launch_bwd_main<D, 128>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
                                          dq_acc, dq_part, part_stride, dk, dv, s);
