@@ -792,6 +792,8 @@ __global__ void fwd_items_fill_kernel(const int32_t* __restrict__ counts, const 
 //   item_off i32  [bh*n]
 //   n_items  i32
 //   items    FwdItem [bh*(ceil(N*width/BM) + n)]
+size_t fwd_ts_item_bytes();
+
 struct FwdWs {
     size_t part_o, part_lse, item_off, n_items, items, total;
 };
@@ -810,10 +812,17 @@ static FwdWs fwd_ws_layout(int64_t bh, int64_t N, int D, int B, int width) {
     w.n_items = off;
     off = align_up(off + 4, 256);
     w.items = off;
-    off = align_up(off + (size_t)bh * (ceil_div(E, kFwdBM) + n) * sizeof(FwdItem), 256);
+    off = align_up(off + (size_t)bh * (ceil_div(E, kFwdBM) + n) * std::max(sizeof(FwdItem), fwd_ts_item_bytes()), 256);
     w.total = off;
     return w;
 }
+
+template <int D>
+int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
+                  const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* item_off,
+                  void* items, const int32_t* n_items, int64_t max_items, float scale_log2, void* part_o,
+                  float* part_lse, cudaStream_t s);
+size_t fwd_ts_item_bytes();
 
 template <int D>
 static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
@@ -826,13 +835,18 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     FwdItem* items = (FwdItem*)(ws + L.items);
     const char* impl = std::getenv("MOBA_FWD_IMPL");
     const bool use_mma = impl != nullptr && impl[0] == 'm';
+    const bool use_ts = ceil_div(B, 16) * 16 <= 128 && (impl == nullptr || impl[0] == 't');
     const int bm = use_mma ? kFwdBM : kTcM;
     fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, bm, item_off, n_items);
-    fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, bm, items);
-    int st = check_launch("fwd_items", 2);
+    if (!use_ts) fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, bm, items);
+    int st = check_launch("fwd_items", use_ts ? 1 : 2);
     if (st) return st;
     const int64_t max_items = bh * (ceil_div(N * width, bm) + n);
-    if (use_mma) {
+    if (use_ts) {
+        st = launch_fwd_ts<D>(q, k, v, bh, N, B, width, counts, offsets, flat, item_off, items, n_items, max_items,
+                              scale * kLog2e, ws + L.part_o, (float*)(ws + L.part_lse), s);
+        if (st) return st;
+    } else if (use_mma) {
         const int BP = (int)ceil_div(B, 64) * 64;
         const size_t smem = (size_t)(kFwdBM + 2 * BP) * D * 2 + kFwdBM * 4;
         auto kern = moba_fwd_mma_kernel<D>;

@@ -1,0 +1,397 @@
+// Forward, ping-pong tcgen05 kernel (moba_forward, src/attention.py:147-182;
+// paper Alg. 1), key-block-major, for block sizes <= 128.
+//
+// Work item = (head, key block j, 128-row tile of block j's varlen slice);
+// items are sorted by (head, block) and every persistent CTA takes a
+// contiguous range, so consecutive items share K_j / V_j. An item record
+// carries everything the roles need (block, tile start in the flat slice,
+// row count), so no role walks a chain of dependent global loads per item.
+//
+//   S(i)  = Q_g K_j^T            SS-MMA  -> TMEM slot i&1 (fp32, BP columns)
+//   P(i)  = exp2(S*scale*log2e - m)      -> bf16 pairs written back over the
+//                                           first BP/2 columns of the slot
+//   O(i)  = P V_j                TS-MMA  (A = P from TMEM, B = V in smem)
+//                                        -> TMEM O buffer i&1
+// Each query row of an item sees the whole (<= 128-key) block at once, so
+// the softmax is single pass (SoftmaxState.update with one chunk,
+// src/attention.py:60-68): row max, exp, sum, and the partial is stored
+// normalised with its LSE; moba_combine merges a query's partials
+// (SoftmaxState.finalize, src/attention.py:70-74).
+//
+// Warps (384 threads):
+//   0      MMA issuer (one lane)
+//   1-3    producers: coalesced cp.async gather of the item's 128 query rows
+//          (8 lanes per 128-B row segment) plus their query ids into smem,
+//          one item of index prefetch ahead; warp 1 lane 0 also loads
+//          K_j / V_j with 3-D TMA (rows past the head's end are zero filled)
+//   4-7    softmax + epilogue for even items   (TMEM lane quadrant warp%4)
+//   8-11   softmax + epilogue for odd items
+// The two softmax warpgroups ping-pong: while one runs exp on item i, the
+// tensor pipe computes S(i+1) / O(i-1) for the other. P never touches
+// shared memory (the SS-MMA of P V would read 32 KB more per item through
+// the smem port than the whole Q gather writes).
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace moba {
+namespace fwdts {
+
+constexpr int kM = 128;
+constexpr int kThreads = 384;
+constexpr int kMma = 0;
+constexpr int kPr0 = 1, kPrN = 3;
+constexpr int kSm0 = 4;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct Bars {
+    uint64_t q_full[4], q_empty[4];
+    uint64_t kv_full[2], kv_empty[2];
+    uint64_t s_full[2], p_full[2], o_full[2];
+    uint32_t tmem;
+};
+
+// hj = head * n_blocks + j; fl = head-local flat position of the tile's
+// first row (offsets[hj] + row0); rows = live rows of the tile (1..128)
+struct __align__(16) Item {
+    int32_t hj, fl, rows, pad;
+};
+
+template <int D>
+struct Cfg {
+    static constexpr int QS = (D == 64) ? 4 : 2;          // Q gather stages
+    static constexpr uint32_t kQBytes = kM * D * 2;
+    static constexpr uint32_t kOCol = 256;                 // O buffers at TMEM cols [256, 256 + 2D)
+};
+
+MOBA_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+MOBA_DEV Item load_item(const Item* p) {
+    int4 v = __ldg(reinterpret_cast<const int4*>(p));
+    return Item{v.x, v.y, v.z, v.w};
+}
+
+// NCH = ceil(BP / 32): 32-column chunks of S the softmax reads
+template <int D, int NCH>
+__global__ void __launch_bounds__(kThreads, 1)
+moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width,
+                   const int32_t* __restrict__ flat, const Item* __restrict__ items,
+                   const int32_t* __restrict__ n_items_ptr, float scale_log2,
+                   __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse) {
+    using namespace sm100;
+    using C = Cfg<D>;
+    constexpr int SL = D / 64;
+    constexpr int QS = C::QS;
+    constexpr int NC = NCH * 32;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t kv_bytes = (uint32_t)BP * D * 2;              // one of K / V
+    const uint32_t oQ = 0, oKV = QS * C::kQBytes;
+    const uint32_t oID = oKV + 4 * kv_bytes;                     // [QS][128] query ids
+    Bars* bars = reinterpret_cast<Bars*>(smem + oID + QS * kM * 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int n_items = *n_items_ptr;
+    const int per = (n_items + gridDim.x - 1) / gridDim.x;
+    const int it0 = min(n_items, (int)blockIdx.x * per);
+    const int n_local = min(n_items, it0 + per) - it0;
+    const Item* my_items = items + it0;
+
+    if (warp == kMma) tmem_alloc(&bars->tmem, 512);
+    if (tid == 0) {
+        for (int s = 0; s < QS; ++s) {
+            mbar_init(&bars->q_full[s], 2 * 32 * kPrN);     // cp.async (noinc) + plain arrival per producer lane
+            mbar_init(&bars->q_empty[s], 1 + 4);            // S MMA commit + the 4 softmax warps (ids read)
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars->kv_full[s], 1);
+            mbar_init(&bars->kv_empty[s], 1);
+            mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->p_full[s], 4);
+            mbar_init(&bars->o_full[s], 1);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem;
+
+    if (n_local > 0) {
+        if (warp == kMma) {
+            // ------------------------------------------------------------ MMA issuer
+            const uint32_t idesc_s = idesc_bf16(kM, BP, false, false);
+            const uint32_t idesc_o = idesc_bf16(kM, D, false, true);
+            int s_hj = -1, s_kv = -1;
+            int kv_of[2] = {0, 0};
+            int hj_next = my_items[0].hj;
+            auto issue_s = [&](int li) {
+                const int hj = hj_next;
+                hj_next = (li + 1 < n_local) ? my_items[li + 1].hj : -1;
+                if (hj != s_hj) {
+                    s_hj = hj;
+                    ++s_kv;
+                    mbar_wait(&bars->kv_full[s_kv & 1], (s_kv >> 1) & 1);
+                }
+                kv_of[li & 1] = s_kv | ((hj_next != hj) ? (1 << 30) : 0);   // bit 30: last use of the K/V buffer
+                const int qs = li % QS;
+                mbar_wait(&bars->q_full[qs], (li / QS) & 1);
+                tc_fence_after();
+                fence_proxy_async_smem();
+                if (lane == 0) {
+                    const uint32_t qa = sbase + oQ + qs * C::kQBytes;
+                    const uint32_t ka = sbase + oKV + (s_kv & 1) * 2 * kv_bytes;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const int sl = kk >> 2, ke = (kk & 3) * 16;
+                        umma_bf16(tmem + (li & 1) * 128, desc_kmajor(qa + sl * kM * 128, ke),
+                                  desc_kmajor(ka + sl * BP * 128, ke), idesc_s, kk > 0);
+                    }
+                    umma_commit(&bars->s_full[li & 1]);
+                    umma_commit(&bars->q_empty[qs]);
+                }
+                __syncwarp();
+            };
+            issue_s(0);
+            if (n_local > 1) issue_s(1);
+            for (int li = 0; li < n_local; ++li) {
+                const int b = li & 1;
+                const int kvu = kv_of[b] & ~(1 << 30);
+                const bool last_use = (kv_of[b] >> 30) & 1;
+                mbar_wait(&bars->p_full[b], (li >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t va = sbase + oKV + (kvu & 1) * 2 * kv_bytes + kv_bytes;
+                    for (int kk = 0; kk < BP / 16; ++kk)
+                        umma_bf16_ts(tmem + C::kOCol + b * D, tmem + b * 128 + 8 * kk,
+                                     desc_mnmajor(va, kk * 16, BP * 128), idesc_o, kk > 0);
+                    umma_commit(&bars->o_full[b]);
+                    if (last_use) umma_commit(&bars->kv_empty[kvu & 1]);
+                }
+                __syncwarp();
+                // S(li+2) reuses slot b: P(li) has been consumed by the O MMA
+                // issued above (tcgen05.mma executes in issue order)
+                if (li + 2 < n_local) issue_s(li + 2);
+            }
+        } else if (warp < kSm0) {
+            // ------------------------------------------------------------ producers
+            const int pw = warp - kPr0;
+            const int sub = lane & 7, rsub = lane >> 3;
+            constexpr int NI = (kM / 4 + kPrN - 1) / kPrN;    // 4-row groups per warp
+            int prev_hj = -1, kv_uses = -1;
+            // rows of this lane: r_i = 4 * (pw + kPrN * i) + rsub; the id of
+            // row r_i is written by the sub == 0 lane
+            auto load_ids = [&](const Item& it, int (&qr)[NI]) {
+                const int32_t* fl = flat + (int64_t)(it.hj / n_blocks) * N * width + it.fl;
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int r = 4 * (pw + kPrN * i) + rsub;
+                    qr[i] = (r < it.rows) ? __ldg(fl + r) : -1;
+                }
+            };
+            Item cur = load_item(my_items);
+            int qrow[NI];
+            load_ids(cur, qrow);
+            for (int li = 0; li < n_local; ++li) {
+                const Item nxt = (li + 1 < n_local) ? load_item(my_items + li + 1) : cur;
+                const int64_t h = cur.hj / n_blocks;
+                const int j = cur.hj - (int)h * n_blocks;
+                if (cur.hj != prev_hj) {
+                    prev_hj = cur.hj;
+                    ++kv_uses;
+                    if (pw == 0 && lane == 0) {
+                        const int ks = kv_uses & 1;
+                        mbar_wait(&bars->kv_empty[ks], ((kv_uses >> 1) & 1) ^ 1);
+                        mbar_expect_tx(&bars->kv_full[ks], 2 * kv_bytes);
+                        const uint32_t kb = sbase + oKV + ks * 2 * kv_bytes;
+#pragma unroll
+                        for (int sl = 0; sl < SL; ++sl) {
+                            tma_load_3d(kb + sl * BP * 128, &tm_k, sl * 64, j * B, (int)h, &bars->kv_full[ks]);
+                            tma_load_3d(kb + kv_bytes + sl * BP * 128, &tm_v, sl * 64, j * B, (int)h,
+                                        &bars->kv_full[ks]);
+                        }
+                    }
+                }
+                const int qs = li % QS;
+                const __nv_bfloat16* Qh = Q + h * N * D;
+                mbar_wait(&bars->q_empty[qs], ((li / QS) & 1) ^ 1);
+                const uint32_t qb = sbase + oQ + qs * C::kQBytes;
+                const uint32_t ib = sbase + oID + qs * kM * 4;
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int r = 4 * (pw + kPrN * i) + rsub;
+                    if (r < kM) {
+                        const int q = qrow[i];
+                        const __nv_bfloat16* src = Qh + (int64_t)max(q, 0) * D + sub * 8;
+                        const uint32_t dst = qb + r * 128 + ((sub ^ (r & 7)) << 4);
+#pragma unroll
+                        for (int sl = 0; sl < SL; ++sl) cp_async16(dst + sl * kM * 128, src + sl * 64, q >= 0);
+                        if (sub == 0) sts32(ib + r * 4, (uint32_t)q);
+                    }
+                }
+                cpasync_arrive_noinc(&bars->q_full[qs]);
+                mbar_arrive(&bars->q_full[qs]);
+                if (li + 1 < n_local) load_ids(nxt, qrow);
+                cur = nxt;
+            }
+        } else {
+            // ------------------------------------------------------------ softmax + epilogue
+            const int wg = (warp - kSm0) >> 2;            // 0: even items, 1: odd items
+            const int quad = warp & 3;
+            const int row = 32 * quad + lane;
+            const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+            const uint32_t slot = tmem + wg * 128 + lane_off;
+            const uint32_t obuf = tmem + C::kOCol + wg * D + lane_off;
+            Item nxt = load_item(my_items + min(wg, n_local - 1));
+            for (int li = wg; li < n_local; li += 2) {
+                const Item cur = nxt;
+                if (li + 2 < n_local) nxt = load_item(my_items + li + 2);
+                const int64_t h = cur.hj / n_blocks;
+                const int64_t k0 = (int64_t)(cur.hj - (int)h * n_blocks) * B;
+                const int64_t pb = h * N * width + cur.fl + row;
+                const bool live = row < cur.rows;
+                const int qs = li % QS;
+                mbar_wait(&bars->s_full[wg], (li >> 1) & 1);
+                tc_fence_after();
+                const int q = lds32i(sbase + oID + qs * kM * 4 + row * 4);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->q_empty[qs]);
+                // visible keys of this row: columns [0, lim); columns
+                // [lim, NC) are masked (past the block end, token-causal in
+                // the own block, or never written by the MMA)
+                const int lim = live ? (int)min64(min64((int64_t)B, N - k0), (int64_t)q - k0 + 1) : 0;
+                float sv[NC];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) tmem_ld32(slot + c * 32, *reinterpret_cast<float(*)[32]>(&sv[c * 32]));
+                tmem_ld_wait();
+                if (lim < NC) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) sv[c] = (c < lim) ? sv[c] : -INFINITY;
+                }
+                float mx[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) mx[u] = sv[u];
+#pragma unroll
+                for (int c = 8; c < NC; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
+                const float m = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                      fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                const float msl = (m == -INFINITY) ? 0.f : m * scale_log2;
+                float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const float p0 = fast_exp2(fmaf(sv[c * 32 + i], scale_log2, -msl));
+                        const float p1 = fast_exp2(fmaf(sv[c * 32 + i + 1], scale_log2, -msl));
+                        ls[(i >> 1) & 3] += p0 + p1;
+                        pk[i >> 1] = pack_bf16(p0, p1);
+                    }
+                    tmem_st16(slot + c * 16, pk);
+                }
+                const float l = (ls[0] + ls[1]) + (ls[2] + ls[3]);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->p_full[wg]);
+                // ---- epilogue: normalised partial O (bf16) and its LSE
+                const float inv = 1.f / l;
+                const float lse = (msl + __log2f(l)) * kLn2;
+                __nv_bfloat16* po = part_o + pb * D;
+                mbar_wait(&bars->o_full[wg], (li >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    float ov[32];
+                    tmem_ld32(obuf + c0, ov);
+                    tmem_ld_wait();
+                    if (live) {
+#pragma unroll
+                        for (int g = 0; g < 4; ++g)
+                            *reinterpret_cast<uint4*>(po + c0 + g * 8) =
+                                make_uint4(pack_bf16(ov[8 * g] * inv, ov[8 * g + 1] * inv),
+                                           pack_bf16(ov[8 * g + 2] * inv, ov[8 * g + 3] * inv),
+                                           pack_bf16(ov[8 * g + 4] * inv, ov[8 * g + 5] * inv),
+                                           pack_bf16(ov[8 * g + 6] * inv, ov[8 * g + 7] * inv));
+                    }
+                }
+                tc_fence_before();
+                if (live) part_lse[pb] = lse;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMma) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// one thread per (head, block): its tiles' item records, at item_off[hj]
+__global__ void fwd_ts_items_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                                    const int32_t* __restrict__ item_off, int64_t total, Item* __restrict__ items) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= total) return;
+    const int cnt = counts[b], off = offsets[b];
+    Item* dst = items + item_off[b];
+    for (int t = 0; t * kM < cnt; ++t) dst[t] = Item{(int32_t)b, off + t * kM, min(kM, cnt - t * kM), 0};
+}
+
+}  // namespace fwdts
+
+bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t heads, uint64_t rows, uint32_t cols,
+                       uint32_t box_rows);
+
+size_t fwd_ts_item_bytes() { return sizeof(fwdts::Item); }
+
+// d in {64, 128}, ceil16(B) <= 128. item_off = exclusive scan of per-(head,
+// block) tile counts (128-row tiles), n_items its total (device).
+template <int D>
+int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
+                  const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* item_off,
+                  void* items, const int32_t* n_items, int64_t max_items, float scale_log2, void* part_o,
+                  float* part_lse, cudaStream_t s) {
+    using namespace fwdts;
+    const int BP = (int)ceil_div(B, 16) * 16;
+    if (BP > 128) return MOBA_ERR_UNSUPPORTED;
+    const int64_t total = bh * ceil_div(N, B);
+    fwd_ts_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, offsets, item_off, total,
+                                                                       (Item*)items);
+    int st = check_launch("fwd_ts_items_kernel");
+    if (st) return st;
+    CUtensorMap tm_k, tm_v;
+    if (!make_tmap_bf16_3d(&tm_k, k, (uint64_t)bh, (uint64_t)N, D, BP) ||
+        !make_tmap_bf16_3d(&tm_v, v, (uint64_t)bh, (uint64_t)N, D, BP))
+        return MOBA_ERR_CUDA;
+    const size_t smem = 1024 + (size_t)Cfg<D>::QS * (Cfg<D>::kQBytes + kM * 4) + 4 * (size_t)BP * D * 2 + sizeof(Bars);
+    if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
+    const int nch = (BP + 31) / 32;
+    auto kern = nch == 1 ? moba_fwd_ts_kernel<D, 1>
+              : nch == 2 ? moba_fwd_ts_kernel<D, 2>
+              : nch == 3 ? moba_fwd_ts_kernel<D, 3>
+                         : moba_fwd_ts_kernel<D, 4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs);
+    StageTimer tm(T_FWD, s);
+    kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, flat,
+                                      (const Item*)items, n_items, scale_log2, (__nv_bfloat16*)part_o, part_lse);
+    return check_launch("moba_fwd_ts_kernel");
+}
+
+template int launch_fwd_ts<64>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,
+                               const int32_t*, const int32_t*, const int32_t*, void*, const int32_t*, int64_t, float,
+                               void*, float*, cudaStream_t);
+template int launch_fwd_ts<128>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,
+                                const int32_t*, const int32_t*, const int32_t*, void*, const int32_t*, int64_t, float,
+                                void*, float*, cudaStream_t);
+
+}  // namespace moba

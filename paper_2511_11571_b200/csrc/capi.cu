@@ -105,6 +105,33 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint32_t 
     return true;
 }
 
+// bf16 [heads, rows, cols] with an SW128 box {64, box_rows, 1}: rows past a
+// head's end are zero filled instead of reading the next head
+bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t heads, uint64_t rows, uint32_t cols,
+                       uint32_t box_rows) {
+    CUtensorMap probe;
+    if (!make_tmap_bf16(&probe, base, rows, cols, box_rows)) return false;   // resolves the driver entry point
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    cuuint64_t dims[3] = {cols, rows, heads};
+    cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)cols * 2 * rows};
+    cuuint32_t box[3] = {64, box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[96];
+        std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
+        set_last_error(buf);
+        return false;
+    }
+    return true;
+}
+
 }  // namespace moba
 
 extern "C" const char* moba_version(void) { return "moba_b200 0.1.0 sm_100a"; }

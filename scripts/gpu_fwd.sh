@@ -1,0 +1,3 @@
+set -x
+timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -5
+timeout 300 python scripts/time_fwd.py t w 2>&1 | tail -12
