@@ -18,35 +18,40 @@
 // normalised with its LSE; moba_combine merges a query's partials
 // (SoftmaxState.finalize, src/attention.py:70-74).
 //
-// Warps (384 threads):
-//   0      MMA issuer (one lane)
+// Warps (512 threads):
+//   0      MMA issuer (one elected lane)
 //   1-3    producers: coalesced cp.async gather of the item's 128 query rows
 //          (8 lanes per 128-B row segment) plus their query ids into smem,
 //          one item of index prefetch ahead; warp 1 lane 0 also loads
 //          K_j / V_j with 3-D TMA (rows past the head's end are zero filled)
-//   4-7    softmax + epilogue for even items   (TMEM lane quadrant warp%4)
-//   8-11   softmax + epilogue for odd items
+//   4-7    softmax for even items   (TMEM lane quadrant warp%4)
+//   8-11   softmax for odd items
+//   12-15  epilogue: O from TMEM -> normalised bf16 partial (TMA store) + LSE
 // The two softmax warpgroups ping-pong: while one runs exp on item i, the
 // tensor pipe computes S(i+1) / O(i-1) for the other. P never touches
 // shared memory (the SS-MMA of P V would read 32 KB more per item through
 // the smem port than the whole Q gather writes).
 #include "common.cuh"
 #include "sm100.cuh"
+#include <cstdio>
+#include <cstdlib>
 
 namespace moba {
 namespace fwdts {
 
 constexpr int kM = 128;
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kMma = 0;
 constexpr int kPr0 = 1, kPrN = 3;
-constexpr int kSm0 = 4;
+constexpr int kSm0 = 4;       // softmax warps 4-11
+constexpr int kEp0 = 12;      // epilogue warps 12-15
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr uint32_t kStg = 32 * 128;    // per-warp O staging: 32 rows x one 64-column SW128 slab
 
 struct Bars {
     uint64_t q_full[4], q_empty[4];
-    uint64_t kv_full[2], kv_empty[2];
-    uint64_t s_full[2], p_full[2], o_full[2];
+    uint64_t kv_full[3], kv_empty[3];
+    uint64_t s_full[2], s_free[2], p_full[2], p_free[2], o_full[2], o_empty[2];
     uint32_t tmem;
 };
 
@@ -60,7 +65,16 @@ template <int D>
 struct Cfg {
     static constexpr int QS = (D == 64) ? 4 : 2;          // Q gather stages
     static constexpr uint32_t kQBytes = kM * D * 2;
-    static constexpr uint32_t kOCol = 256;                 // O buffers at TMEM cols [256, 256 + 2D)
+    // d = 64: S, P and O each have their own TMEM columns, so S(i+2) can be
+    // issued as soon as the softmax has read S(i) (before P(i) is consumed):
+    //   S [0, 256)  P [256, 384)  O [384, 512)
+    // d = 128: P aliases the first half of its S slot (S(i+2) waits for the
+    // O MMA of item i):   S/P [0, 256)  O [256, 512)
+    static constexpr bool kSplit = (D == 64);
+    static constexpr int KVS = kSplit ? 3 : 2;             // K/V stages (S runs up to 2 items ahead)
+    static constexpr uint32_t kPCol = kSplit ? 256 : 0;
+    static constexpr uint32_t kPStride = kSplit ? 64 : 128;
+    static constexpr uint32_t kOCol = kSplit ? 384 : 256;
 };
 
 MOBA_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
@@ -83,9 +97,15 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                    const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width,
                    const int32_t* __restrict__ flat, const Item* __restrict__ items,
                    const int32_t* __restrict__ n_items_ptr, float scale_log2,
-                   __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse) {
+                   __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse,
+                   const __grid_constant__ CUtensorMap tm_po, long long* __restrict__ trace) {
     using namespace sm100;
     using C = Cfg<D>;
+    // debug timeline (MOBA_FWD_TRACE): CTA 0, lane 0 of the recording warp
+#define TR(li, ev)                                                                          \
+    do {                                                                                    \
+        if (trace != nullptr && blockIdx.x == 0 && lane == 0 && (li) < 256) trace[(li) * 16 + (ev)] = clock64(); \
+    } while (0)
     constexpr int SL = D / 64;
     constexpr int QS = C::QS;
     constexpr int NC = NCH * 32;
@@ -94,8 +114,10 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
     const uint32_t sbase = smem_u32(smem);
     const uint32_t kv_bytes = (uint32_t)BP * D * 2;              // one of K / V
     const uint32_t oQ = 0, oKV = QS * C::kQBytes;
-    const uint32_t oID = oKV + 4 * kv_bytes;                     // [QS][128] query ids
-    Bars* bars = reinterpret_cast<Bars*>(smem + oID + QS * kM * 4);
+    const uint32_t oSTG = oKV + C::KVS * 2 * kv_bytes;           // [4 epilogue warps][32 rows][128 B] O staging
+    const uint32_t oID = oSTG + 4 * kStg;                        // [QS][128] query ids
+    const uint32_t oST = oID + QS * kM * 4;                      // [4][128] (1/l, lse) per row
+    Bars* bars = reinterpret_cast<Bars*>(smem + oST + 4 * kM * 8);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_blocks = (int)((N + B - 1) / B);
@@ -111,12 +133,17 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
             mbar_init(&bars->q_full[s], 2 * 32 * kPrN);     // cp.async (noinc) + plain arrival per producer lane
             mbar_init(&bars->q_empty[s], 1 + 4);            // S MMA commit + the 4 softmax warps (ids read)
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < C::KVS; ++s) {
             mbar_init(&bars->kv_full[s], 1);
             mbar_init(&bars->kv_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&bars->s_full[s], 1);
+            mbar_init(&bars->s_free[s], 4);
+            mbar_init(&bars->p_free[s], 1);
             mbar_init(&bars->p_full[s], 4);
             mbar_init(&bars->o_full[s], 1);
+            mbar_init(&bars->o_empty[s], 4);
         }
         fence_mbar_init();
     }
@@ -125,63 +152,10 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem = bars->tmem;
 
-    if (n_local > 0) {
-        if (warp == kMma) {
-            // ------------------------------------------------------------ MMA issuer
-            const uint32_t idesc_s = idesc_bf16(kM, BP, false, false);
-            const uint32_t idesc_o = idesc_bf16(kM, D, false, true);
-            int s_hj = -1, s_kv = -1;
-            int kv_of[2] = {0, 0};
-            int hj_next = my_items[0].hj;
-            auto issue_s = [&](int li) {
-                const int hj = hj_next;
-                hj_next = (li + 1 < n_local) ? my_items[li + 1].hj : -1;
-                if (hj != s_hj) {
-                    s_hj = hj;
-                    ++s_kv;
-                    mbar_wait(&bars->kv_full[s_kv & 1], (s_kv >> 1) & 1);
-                }
-                kv_of[li & 1] = s_kv | ((hj_next != hj) ? (1 << 30) : 0);   // bit 30: last use of the K/V buffer
-                const int qs = li % QS;
-                mbar_wait(&bars->q_full[qs], (li / QS) & 1);
-                tc_fence_after();
-                fence_proxy_async_smem();
-                if (lane == 0) {
-                    const uint32_t qa = sbase + oQ + qs * C::kQBytes;
-                    const uint32_t ka = sbase + oKV + (s_kv & 1) * 2 * kv_bytes;
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const int sl = kk >> 2, ke = (kk & 3) * 16;
-                        umma_bf16(tmem + (li & 1) * 128, desc_kmajor(qa + sl * kM * 128, ke),
-                                  desc_kmajor(ka + sl * BP * 128, ke), idesc_s, kk > 0);
-                    }
-                    umma_commit(&bars->s_full[li & 1]);
-                    umma_commit(&bars->q_empty[qs]);
-                }
-                __syncwarp();
-            };
-            issue_s(0);
-            if (n_local > 1) issue_s(1);
-            for (int li = 0; li < n_local; ++li) {
-                const int b = li & 1;
-                const int kvu = kv_of[b] & ~(1 << 30);
-                const bool last_use = (kv_of[b] >> 30) & 1;
-                mbar_wait(&bars->p_full[b], (li >> 1) & 1);
-                tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t va = sbase + oKV + (kvu & 1) * 2 * kv_bytes + kv_bytes;
-                    for (int kk = 0; kk < BP / 16; ++kk)
-                        umma_bf16_ts(tmem + C::kOCol + b * D, tmem + b * 128 + 8 * kk,
-                                     desc_mnmajor(va, kk * 16, BP * 128), idesc_o, kk > 0);
-                    umma_commit(&bars->o_full[b]);
-                    if (last_use) umma_commit(&bars->kv_empty[kvu & 1]);
-                }
-                __syncwarp();
-                // S(li+2) reuses slot b: P(li) has been consumed by the O MMA
-                // issued above (tcgen05.mma executes in issue order)
-                if (li + 2 < n_local) issue_s(li + 2);
-            }
-        } else if (warp < kSm0) {
+    // register budget (setmaxnreg per warpgroup, executed before the roles
+    // diverge): 128 x 104 (MMA + producers) + 256 x 168 (softmax) + 128 x 72
+    // (epilogue) = 64K
+    auto run_producer = [&]() {
             // ------------------------------------------------------------ producers
             const int pw = warp - kPr0;
             const int sub = lane & 7, rsub = lane >> 3;
@@ -208,8 +182,8 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                     prev_hj = cur.hj;
                     ++kv_uses;
                     if (pw == 0 && lane == 0) {
-                        const int ks = kv_uses & 1;
-                        mbar_wait(&bars->kv_empty[ks], ((kv_uses >> 1) & 1) ^ 1);
+                        const int ks = kv_uses % C::KVS;
+                        mbar_wait(&bars->kv_empty[ks], ((kv_uses / C::KVS) & 1) ^ 1);
                         mbar_expect_tx(&bars->kv_full[ks], 2 * kv_bytes);
                         const uint32_t kb = sbase + oKV + ks * 2 * kv_bytes;
 #pragma unroll
@@ -222,7 +196,9 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 }
                 const int qs = li % QS;
                 const __nv_bfloat16* Qh = Q + h * N * D;
+                if (pw == 0) TR(li, 4);
                 mbar_wait(&bars->q_empty[qs], ((li / QS) & 1) ^ 1);
+                if (pw == 0) TR(li, 5);
                 const uint32_t qb = sbase + oQ + qs * C::kQBytes;
                 const uint32_t ib = sbase + oID + qs * kM * 4;
 #pragma unroll
@@ -239,27 +215,111 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 }
                 cpasync_arrive_noinc(&bars->q_full[qs]);
                 mbar_arrive(&bars->q_full[qs]);
+                if (pw == 0) TR(li, 6);
                 if (li + 1 < n_local) load_ids(nxt, qrow);
                 cur = nxt;
             }
-        } else {
-            // ------------------------------------------------------------ softmax + epilogue
+    };
+
+    if (warp < kSm0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+        if (n_local > 0 && warp == kMma) {
+            // ------------------------------------------------------------ MMA issuer
+            // warp-uniform: every lane runs the loop, one elected lane issues;
+            // descriptors advance by constants (start address field, 16 B units)
+            const uint32_t idesc_s = idesc_bf16(kM, BP, false, false);
+            const uint32_t idesc_o = idesc_bf16(kM, D, false, true);
+            int s_hj = -1, s_kv = -1;
+            int kv_of[4] = {0, 0, 0, 0};
+            // block ids of items li, li+1, li+2 (loaded two issues ahead)
+            int hj0 = my_items[0].hj;
+            int hj1 = n_local > 1 ? my_items[1].hj : -1;
+            int hj2 = n_local > 2 ? my_items[2].hj : -1;
+            auto issue_s = [&](int li) {
+                const int hj = hj0;
+                const bool last = hj1 != hj;
+                hj0 = hj1;
+                hj1 = hj2;
+                hj2 = (li + 3 < n_local) ? my_items[li + 3].hj : -1;
+                if (hj != s_hj) {
+                    s_hj = hj;
+                    ++s_kv;
+                    mbar_wait(&bars->kv_full[s_kv % C::KVS], (s_kv / C::KVS) & 1);
+                }
+                kv_of[li & 3] = s_kv | (last ? (1 << 30) : 0);   // bit 30: last use of the K/V buffer
+                const int qs = li % QS;
+                TR(li, 0);
+                mbar_wait(&bars->q_full[qs], (li / QS) & 1);
+                TR(li, 1);
+                tc_fence_after();
+                fence_proxy_async_smem();
+                const uint64_t dq = desc_kmajor(sbase + oQ + qs * C::kQBytes, 0);
+                const uint64_t dk = desc_kmajor(sbase + oKV + (s_kv % C::KVS) * 2 * kv_bytes, 0);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const int sl = kk >> 2, ke = kk & 3;
+                    umma_bf16_w(tmem + (li & 1) * 128, dq + (uint64_t)(sl * (kM * 128 >> 4) + ke * 2),
+                                dk + (uint64_t)(sl * (BP * 128 >> 4) + ke * 2), idesc_s, kk > 0);
+                }
+                umma_commit_w(&bars->s_full[li & 1]);
+                umma_commit_w(&bars->q_empty[qs]);
+                TR(li, 13);
+            };
+            issue_s(0);
+            if (n_local > 1) issue_s(1);
+            for (int li = 0; li < n_local; ++li) {
+                const int b = li & 1;
+                if (C::kSplit && li + 2 < n_local) {
+                    // S(li+2) goes into slot b once the softmax has read S(li)
+                    mbar_wait(&bars->s_free[b], (li >> 1) & 1);
+                    issue_s(li + 2);
+                }
+                const int kvu = kv_of[li & 3] & ~(1 << 30);
+                const bool last_use = (kv_of[li & 3] >> 30) & 1;
+                TR(li, 2);
+                mbar_wait(&bars->p_full[b], (li >> 1) & 1);
+                mbar_wait(&bars->o_empty[b], ((li >> 1) & 1) ^ 1);
+                TR(li, 3);
+                tc_fence_after();
+                const uint64_t dv = desc_mnmajor(sbase + oKV + (kvu % C::KVS) * 2 * kv_bytes + kv_bytes, 0, BP * 128);
+                const uint32_t ta = tmem + C::kPCol + b * C::kPStride;
+                for (int kk = 0; kk < BP / 16; ++kk)
+                    umma_bf16_ts_w(tmem + C::kOCol + b * D, ta + 8 * kk, dv + (uint64_t)(kk * 128), idesc_o, kk > 0);
+                umma_commit_w(&bars->o_full[b]);
+                umma_commit_w(&bars->p_free[b]);
+                if (last_use) umma_commit_w(&bars->kv_empty[kvu % C::KVS]);
+                TR(li, 12);
+                // d = 128: S(li+2) reuses slot b, whose P(li) has been consumed
+                // by the O MMA issued above (tcgen05.mma executes in issue order)
+                if (!C::kSplit && li + 2 < n_local) issue_s(li + 2);
+            }
+        } else if (n_local > 0) {
+            run_producer();
+        }
+    } else if (warp < kEp0) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
+        if (n_local > 0) {
+            // ------------------------------------------------------------ softmax
+            // a thread holds its whole S row (setmaxnreg gives these two
+            // warpgroups 168 registers, taken from the producer/MMA and
+            // epilogue warpgroups)
             const int wg = (warp - kSm0) >> 2;            // 0: even items, 1: odd items
             const int quad = warp & 3;
             const int row = 32 * quad + lane;
             const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
             const uint32_t slot = tmem + wg * 128 + lane_off;
-            const uint32_t obuf = tmem + C::kOCol + wg * D + lane_off;
+            const uint32_t pslot = tmem + C::kPCol + wg * C::kPStride + lane_off;
             Item nxt = load_item(my_items + min(wg, n_local - 1));
             for (int li = wg; li < n_local; li += 2) {
                 const Item cur = nxt;
                 if (li + 2 < n_local) nxt = load_item(my_items + li + 2);
                 const int64_t h = cur.hj / n_blocks;
                 const int64_t k0 = (int64_t)(cur.hj - (int)h * n_blocks) * B;
-                const int64_t pb = h * N * width + cur.fl + row;
                 const bool live = row < cur.rows;
                 const int qs = li % QS;
+                if (quad == 0) TR(li, 7);
                 mbar_wait(&bars->s_full[wg], (li >> 1) & 1);
+                if (quad == 0) TR(li, 8);
                 tc_fence_after();
                 const int q = lds32i(sbase + oID + qs * kM * 4 + row * 4);
                 __syncwarp();
@@ -268,11 +328,17 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 // [lim, NC) are masked (past the block end, token-causal in
                 // the own block, or never written by the MMA)
                 const int lim = live ? (int)min64(min64((int64_t)B, N - k0), (int64_t)q - k0 + 1) : 0;
+                const bool masked = lim < NC;
                 float sv[NC];
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) tmem_ld32(slot + c * 32, *reinterpret_cast<float(*)[32]>(&sv[c * 32]));
                 tmem_ld_wait();
-                if (lim < NC) {
+                if (C::kSplit) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->s_free[wg]);
+                }
+                if (masked) {
 #pragma unroll
                     for (int c = 0; c < NC; ++c) sv[c] = (c < lim) ? sv[c] : -INFINITY;
                 }
@@ -284,6 +350,11 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 const float m = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
                 const float msl = (m == -INFINITY) ? 0.f : m * scale_log2;
+                // P slot b is free once the O MMA of item li - 2 has run
+                if (C::kSplit && li >= 2) {
+                    mbar_wait(&bars->p_free[wg], ((li >> 1) - 1) & 1);
+                    tc_fence_after();
+                }
                 float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
@@ -295,37 +366,100 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                         ls[(i >> 1) & 3] += p0 + p1;
                         pk[i >> 1] = pack_bf16(p0, p1);
                     }
-                    tmem_st16(slot + c * 16, pk);
+                    tmem_st16(pslot + c * 16, pk);
                 }
                 const float l = (ls[0] + ls[1]) + (ls[2] + ls[3]);
+                // row statistics for the epilogue warps (slot li & 3: the
+                // epilogue of li has read them before S(li + 4) can exist)
+                {
+                    const uint32_t st = sbase + oST + ((li & 3) * kM + row) * 8;
+                    asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(st), "f"(1.f / l),
+                                 "f"((msl + __log2f(l)) * kLn2)
+                                 : "memory");
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[wg]);
-                // ---- epilogue: normalised partial O (bf16) and its LSE
-                const float inv = 1.f / l;
-                const float lse = (msl + __log2f(l)) * kLn2;
-                __nv_bfloat16* po = part_o + pb * D;
-                mbar_wait(&bars->o_full[wg], (li >> 1) & 1);
+                if (quad == 0) TR(li, 9);
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+        if (n_local > 0) {
+            // ------------------------------------------------------------ epilogue
+            // normalised partial O (bf16) and its LSE. A warp whose 32 rows
+            // are all live stages them in SW128 smem and writes 4 KB per slab
+            // with one TMA store (the rows are contiguous flat positions); the
+            // tail warp of a block's last tile stores its live rows directly.
+            const int quad = warp & 3;
+            const int row = 32 * quad + lane;
+            const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+            const uint32_t stg = sbase + oSTG + quad * kStg;
+            Item nxt = load_item(my_items);
+            for (int li = 0; li < n_local; ++li) {
+                const Item cur = nxt;
+                if (li + 1 < n_local) nxt = load_item(my_items + li + 1);
+                const int b = li & 1;
+                const int64_t pb = (int64_t)(cur.hj / n_blocks) * N * width + cur.fl + row;
+                const bool live = row < cur.rows;
+                const bool full_warp = 32 * quad + 32 <= cur.rows;
+                const uint32_t obuf = tmem + C::kOCol + b * D + lane_off;
+                mbar_wait(&bars->o_full[b], (li >> 1) & 1);
+                if (quad == 0) TR(li, 10);
                 tc_fence_after();
+                float st0, st1;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
+                             : "=f"(st0), "=f"(st1)
+                             : "r"(sbase + oST + ((li & 3) * kM + row) * 8));
+                const float inv = st0;
+                if (live) part_lse[pb] = st1;
 #pragma unroll
-                for (int c0 = 0; c0 < D; c0 += 32) {
-                    float ov[32];
-                    tmem_ld32(obuf + c0, ov);
-                    tmem_ld_wait();
-                    if (live) {
+                for (int sl = 0; sl < SL; ++sl) {
+                    if (full_warp) {
+                        if (lane == 0) bulk_wait_read0();            // previous store has read the staging slab
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        float ov[32];
+                        tmem_ld32(obuf + sl * 64 + hh * 32, ov);
+                        tmem_ld_wait();
+                        if (sl == SL - 1 && hh == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&bars->o_empty[b]);
+                        }
+                        uint4 pk[4];
 #pragma unroll
                         for (int g = 0; g < 4; ++g)
-                            *reinterpret_cast<uint4*>(po + c0 + g * 8) =
-                                make_uint4(pack_bf16(ov[8 * g] * inv, ov[8 * g + 1] * inv),
-                                           pack_bf16(ov[8 * g + 2] * inv, ov[8 * g + 3] * inv),
-                                           pack_bf16(ov[8 * g + 4] * inv, ov[8 * g + 5] * inv),
-                                           pack_bf16(ov[8 * g + 6] * inv, ov[8 * g + 7] * inv));
+                            pk[g] = make_uint4(pack_bf16(ov[8 * g] * inv, ov[8 * g + 1] * inv),
+                                               pack_bf16(ov[8 * g + 2] * inv, ov[8 * g + 3] * inv),
+                                               pack_bf16(ov[8 * g + 4] * inv, ov[8 * g + 5] * inv),
+                                               pack_bf16(ov[8 * g + 6] * inv, ov[8 * g + 7] * inv));
+                        if (full_warp) {
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+                                sts128(stg + lane * 128 + (((hh * 4 + g) ^ (lane & 7)) << 4), pk[g]);
+                        } else if (live) {
+                            __nv_bfloat16* po = part_o + pb * D + sl * 64 + hh * 32;
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint4*>(po + g * 8) = pk[g];
+                        }
+                    }
+                    if (quad == 0 && sl == 0) TR(li, 14);
+                    if (full_warp) {
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tm_po, stg, sl * 64, (int)(pb - lane));
+                            bulk_commit();
+                        }
                     }
                 }
-                tc_fence_before();
-                if (live) part_lse[pb] = lse;
+                if (quad == 0) TR(li, 11);
             }
+            if (lane == 0) bulk_wait0();
         }
     }
     tc_fence_before();
@@ -372,7 +506,10 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
     if (!make_tmap_bf16_3d(&tm_k, k, (uint64_t)bh, (uint64_t)N, D, BP) ||
         !make_tmap_bf16_3d(&tm_v, v, (uint64_t)bh, (uint64_t)N, D, BP))
         return MOBA_ERR_CUDA;
-    const size_t smem = 1024 + (size_t)Cfg<D>::QS * (Cfg<D>::kQBytes + kM * 4) + 4 * (size_t)BP * D * 2 + sizeof(Bars);
+    CUtensorMap tm_po;
+    if (!make_tmap_bf16(&tm_po, part_o, (uint64_t)(bh * N * width), D, 32)) return MOBA_ERR_CUDA;
+    const size_t smem = 1024 + (size_t)Cfg<D>::QS * (Cfg<D>::kQBytes + kM * 4) + 2 * Cfg<D>::KVS * (size_t)BP * D * 2 + 4 * kStg +
+                        4 * kM * 8 + sizeof(Bars);
     if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
     const int nch = (BP + 31) / 32;
     auto kern = nch == 1 ? moba_fwd_ts_kernel<D, 1>
@@ -381,10 +518,27 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
                          : moba_fwd_ts_kernel<D, 4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs);
-    StageTimer tm(T_FWD, s);
-    kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, flat,
-                                      (const Item*)items, n_items, scale_log2, (__nv_bfloat16*)part_o, part_lse);
-    return check_launch("moba_fwd_ts_kernel");
+    static long long* trace = nullptr;
+    const char* trace_path = std::getenv("MOBA_FWD_TRACE");
+    if (trace_path != nullptr && trace == nullptr) cudaMalloc(&trace, 256 * 16 * sizeof(long long));
+    if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
+    {
+        StageTimer tm(T_FWD, s);
+        kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, flat,
+                                          (const Item*)items, n_items, scale_log2, (__nv_bfloat16*)part_o, part_lse, tm_po,
+                                          trace_path != nullptr ? trace : nullptr);
+    }
+    st = check_launch("moba_fwd_ts_kernel");
+    if (st == 0 && trace_path != nullptr) {
+        static long long host[256 * 16];
+        cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            std::fwrite(host, sizeof(host), 1, f);
+            std::fclose(f);
+        }
+    }
+    return st;
 }
 
 template int launch_fwd_ts<64>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,

@@ -214,6 +214,42 @@ MOBA_DEV void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// Warp-uniform variants: the whole warp executes the call and one elected
+// lane issues the instruction (elect.sync inside the asm), so the compiler
+// keeps descriptors in uniform registers instead of wrapping each MMA in a
+// divergent single-lane region.
+MOBA_DEV void umma_bf16_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"((uint32_t)accumulate));
+}
+MOBA_DEV void umma_bf16_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"((uint32_t)accumulate));
+}
+MOBA_DEV void umma_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// 2-D tiled store of an SW128 box {64, rows} from smem (bulk-group completion)
+MOBA_DEV void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int row) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
+                 "r"(row), "r"(src)
+                 : "memory");
+}
+
 // byte offset of element (row, col) in an SW128 tile with `rows` rows per slab
 MOBA_DEV uint32_t sw128_off(int row, int col, int rows) {
     int slab = col >> 6;
