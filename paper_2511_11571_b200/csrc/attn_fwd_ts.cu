@@ -355,16 +355,25 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                     mbar_wait(&bars->p_free[wg], ((li >> 1) - 1) & 1);
                     tc_fence_after();
                 }
+                // x*scale - m and the row sum in packed fp32x2 (FFMA2 / FADD2)
                 float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
                     uint32_t pk[16];
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const float p0 = fast_exp2(fmaf(sv[c * 32 + i], scale_log2, -msl));
-                        const float p1 = fast_exp2(fmaf(sv[c * 32 + i + 1], scale_log2, -msl));
-                        ls[(i >> 1) & 3] += p0 + p1;
-                        pk[i >> 1] = pack_bf16(p0, p1);
+                    for (int i = 0; i < 32; i += 4) {
+                        float t0, t1, t2, t3;
+                        ffma2(t0, t1, sv[c * 32 + i], sv[c * 32 + i + 1], scale_log2, scale_log2, -msl, -msl);
+                        ffma2(t2, t3, sv[c * 32 + i + 2], sv[c * 32 + i + 3], scale_log2, scale_log2, -msl, -msl);
+                        t0 = fast_exp2(t0);
+                        t1 = fast_exp2(t1);
+                        t2 = fast_exp2(t2);
+                        t3 = fast_exp2(t3);
+                        const int a = (i >> 1) & 2;
+                        fadd2(ls[a], ls[a + 1], ls[a], ls[a + 1], t0, t1);
+                        fadd2(ls[a], ls[a + 1], ls[a], ls[a + 1], t2, t3);
+                        pk[i >> 1] = pack_bf16(t0, t1);
+                        pk[(i >> 1) + 1] = pack_bf16(t2, t3);
                     }
                     tmem_st16(pslot + c * 16, pk);
                 }
