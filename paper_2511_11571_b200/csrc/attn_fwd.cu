@@ -689,52 +689,96 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 }
 
 // ---------------------------------------------------------------- combine
-// One warp per query: merge its <= width partials (lse-weighted).
-template <int D>
-__global__ void moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_lse,
-                                    const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t total_rows,
-                                    __nv_bfloat16* __restrict__ O, float* __restrict__ LSE) {
-    constexpr int PER = D / 32;  // channels per lane
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// One warp per query: merge its <= width partials (lse-weighted,
+// SoftmaxState.finalize over the query's blocks, src/attention.py:70-74).
+// A partial row (D bf16) is read by L = D/8 lanes with 16-B loads, so one
+// warp instruction fetches 32/L partial rows; all rounds are issued before
+// any is consumed. The lane groups are then reduced with shuffles and the
+// first L lanes write the row (coalesced).
+template <int D, int WMAX>
+__global__ void __launch_bounds__(256)
+moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_lse,
+                    const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t total_rows,
+                    __nv_bfloat16* __restrict__ O, float* __restrict__ LSE) {
+    constexpr int L = D / 8;               // lanes per partial row
+    constexpr int G = 32 / L;              // partial rows per warp instruction
+    constexpr int R = (WMAX + G - 1) / G;  // load rounds per query
+    constexpr int QW = 2;                  // queries per warp, loads of both in flight together
+    const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * QW;
     const int lane = threadIdx.x & 31;
-    if (row >= total_rows) return;
-    const int64_t h = row / N;
-    const int32_t* rp = row_pos + row * width;
-    int32_t p = (lane < width) ? rp[lane] : -1;
-    float ls = (p >= 0) ? part_lse[h * N * width + p] : -INFINITY;
-    float m = warp_max(ls);
-    float w = (p >= 0) ? __expf(ls - m) : 0.f;
-    float wsum = warp_sum(w);
-    float acc[PER];
+    if (row0 >= total_rows) return;
+    const int grp = lane / L, sub = lane % L;
+    int32_t p[QW];
 #pragma unroll
-    for (int c = 0; c < PER; ++c) acc[c] = 0.f;
-    for (int s = 0; s < width; ++s) {
-        int32_t ps = __shfl_sync(0xffffffffu, p, s);
-        float ws = __shfl_sync(0xffffffffu, w, s);
-        if (ps < 0) continue;
-        const __nv_bfloat16* src = part_o + (h * N * width + ps) * D + lane * PER;
-        if constexpr (PER == 2) {
-            float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(src));
-            acc[0] = fmaf(ws, f.x, acc[0]);
-            acc[1] = fmaf(ws, f.y, acc[1]);
-        } else {
-            uint2 u = *reinterpret_cast<const uint2*>(src);
-            float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y);
-            acc[0] = fmaf(ws, f0.x, acc[0]);
-            acc[1] = fmaf(ws, f0.y, acc[1]);
-            acc[2] = fmaf(ws, f1.x, acc[2]);
-            acc[3] = fmaf(ws, f1.y, acc[3]);
+    for (int t = 0; t < QW; ++t)
+        p[t] = (lane < width && row0 + t < total_rows) ? __ldg(row_pos + (row0 + t) * width + lane) : -1;
+    float ls[QW];
+    uint4 raw[QW][R];
+    int32_t pr[QW][R];
+#pragma unroll
+    for (int t = 0; t < QW; ++t) {
+        const int64_t h = (row0 + t) / N;
+        ls[t] = (p[t] >= 0) ? __ldg(part_lse + h * N * width + p[t]) : -INFINITY;
+        const uint4* base = reinterpret_cast<const uint4*>(part_o + h * N * width * D) + sub;
+        const int32_t p0 = max(__shfl_sync(0xffffffffu, p[t], 0), 0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            pr[t][r] = __shfl_sync(0xffffffffu, p[t], (r * G + grp) & 31);
+            if (r * G + grp >= width) pr[t][r] = -1;
+            raw[t][r] = __ldg(base + (int64_t)(pr[t][r] >= 0 ? pr[t][r] : p0) * L);
         }
     }
-    const float inv = 1.f / wsum;
-    __nv_bfloat16* dst = O + row * D + lane * PER;
-    if constexpr (PER == 2) {
-        *reinterpret_cast<uint32_t*>(dst) = pack_bf16(acc[0] * inv, acc[1] * inv);
-    } else {
-        *reinterpret_cast<uint2*>(dst) =
-            make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+#pragma unroll
+    for (int t = 0; t < QW; ++t) {
+        const int64_t row = row0 + t;
+        const float m = warp_max(ls[t]);
+        const float w = (p[t] >= 0) ? __expf(ls[t] - m) : 0.f;
+        const float wsum = warp_sum(w);
+        float acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float wt = __shfl_sync(0xffffffffu, w, (r * G + grp) & 31);
+            if (pr[t][r] < 0) wt = 0.f;
+            const uint32_t u[4] = {raw[t][r].x, raw[t][r].y, raw[t][r].z, raw[t][r].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float2 f = unpack_bf16(u[c]);
+                acc[2 * c] = fmaf(wt, f.x, acc[2 * c]);
+                acc[2 * c + 1] = fmaf(wt, f.y, acc[2 * c + 1]);
+            }
+        }
+#pragma unroll
+        for (int o = L; o < 32; o <<= 1)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        if (row < total_rows) {
+            const float inv = 1.f / wsum;
+            if (grp == 0) {
+                uint4 outv = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                                        pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+                *(reinterpret_cast<uint4*>(O + row * D) + sub) = outv;
+            }
+            if (lane == 0) LSE[row] = m + __logf(wsum);
+        }
     }
-    if (lane == 0) LSE[row] = m + __logf(wsum);
+}
+
+template <int D>
+static void launch_combine(const void* part_o, const float* part_lse, const int32_t* row_pos, int64_t N, int width,
+                           int64_t rows, void* out, float* lse, cudaStream_t s) {
+    const unsigned grid = (unsigned)ceil_div(rows, 8 * 2);
+    auto po = (const __nv_bfloat16*)part_o;
+    auto o = (__nv_bfloat16*)out;
+#define MOBA_COMBINE(W) moba_combine_kernel<D, W><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, rows, o, lse)
+    if (width <= 4) MOBA_COMBINE(4);
+    else if (width <= 8) MOBA_COMBINE(8);
+    else if (width <= 12) MOBA_COMBINE(12);
+    else if (width <= 16) MOBA_COMBINE(16);
+    else if (width <= 24) MOBA_COMBINE(24);
+    else MOBA_COMBINE(32);
+#undef MOBA_COMBINE
 }
 
 // ---------------------------------------------------------------- work items
@@ -819,9 +863,10 @@ static FwdWs fwd_ws_layout(int64_t bh, int64_t N, int D, int B, int width) {
 
 template <int D>
 int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
-                  const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* item_off,
-                  void* items, const int32_t* n_items, int64_t max_items, float scale_log2, void* part_o,
-                  float* part_lse, cudaStream_t s);
+                  const int32_t* flat, const void* items, const int32_t* item_lo, const int32_t* item_hi,
+                  float scale_log2, void* part_o, float* part_lse, cudaStream_t s);
+void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int32_t* item_off, int64_t total,
+                       void* items, cudaStream_t s);
 size_t fwd_ts_item_bytes();
 
 template <int D>
@@ -843,9 +888,32 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     if (st) return st;
     const int64_t max_items = bh * (ceil_div(N * width, bm) + n);
     if (use_ts) {
-        st = launch_fwd_ts<D>(q, k, v, bh, N, B, width, counts, offsets, flat, item_off, items, n_items, max_items,
-                              scale * kLog2e, ws + L.part_o, (float*)(ws + L.part_lse), s);
+        // heads in chunks whose partials (<= 48 MB) stay in L2 until the
+        // chunk's combine reads them back
+        fwd_ts_fill_items(counts, offsets, item_off, total, items, s);
+        st = check_launch("fwd_ts_items_kernel");
         if (st) return st;
+        const int64_t per_head = N * width * (int64_t)D * 2;
+        // (measured: smaller fwd launches cost more in pipeline ramp-up than the
+        // combine saves, so by default all heads form one chunk)
+        const char* chunk_env = std::getenv("MOBA_FWD_CHUNK_MB");
+        const int64_t chunk_mb = chunk_env ? std::atoll(chunk_env) : 0;
+        const int64_t hc = chunk_mb > 0 ? std::max<int64_t>(1, (chunk_mb << 20) / per_head) : bh;
+        for (int64_t h0 = 0; h0 < bh; h0 += hc) {
+            const int64_t h1 = std::min(bh, h0 + hc);
+            const int32_t* lo = item_off + h0 * n;
+            const int32_t* hi = h1 < bh ? item_off + h1 * n : n_items;
+            st = launch_fwd_ts<D>(q, k, v, bh, N, B, width, flat, items, lo, hi, scale * kLog2e, ws + L.part_o,
+                                  (float*)(ws + L.part_lse), s);
+            if (st) return st;
+            StageTimer tm(T_COMBINE, s);
+            launch_combine<D>(ws + L.part_o + h0 * N * width * D * 2, (const float*)(ws + L.part_lse) + h0 * N * width,
+                              row_pos + h0 * N * width, N, width, (h1 - h0) * N, (uint8_t*)out + h0 * N * D * 2,
+                              lse + h0 * N, s);
+            st = check_launch("moba_combine_kernel");
+            if (st) return st;
+        }
+        return MOBA_OK;
     } else if (use_mma) {
         const int BP = (int)ceil_div(B, 64) * 64;
         const size_t smem = (size_t)(kFwdBM + 2 * BP) * D * 2 + kFwdBM * 4;
@@ -903,9 +971,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     if (st) return st;
     StageTimer tm(T_COMBINE, s);
     const int64_t rows = bh * N;
-    moba_combine_kernel<D><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(
-        (const __nv_bfloat16*)(ws + L.part_o), (const float*)(ws + L.part_lse), row_pos, N, width, rows,
-        (__nv_bfloat16*)out, lse);
+    launch_combine<D>(ws + L.part_o, (const float*)(ws + L.part_lse), row_pos, N, width, rows, out, lse, s);
     return check_launch("moba_combine_kernel");
 }
 

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width,
                    const int32_t* __restrict__ flat, const Item* __restrict__ items,
-                   const int32_t* __restrict__ n_items_ptr, float scale_log2,
+                   const int32_t* __restrict__ item_lo, const int32_t* __restrict__ item_hi, float scale_log2,
                    __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse,
                    const __grid_constant__ CUtensorMap tm_po, long long* __restrict__ trace) {
     using namespace sm100;
@@ -121,11 +121,12 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_blocks = (int)((N + B - 1) / B);
-    const int n_items = *n_items_ptr;
+    const int lo = *item_lo;
+    const int n_items = *item_hi - lo;
     const int per = (n_items + gridDim.x - 1) / gridDim.x;
     const int it0 = min(n_items, (int)blockIdx.x * per);
     const int n_local = min(n_items, it0 + per) - it0;
-    const Item* my_items = items + it0;
+    const Item* my_items = items + lo + it0;
 
     if (warp == kMma) tmem_alloc(&bars->tmem, 512);
     if (tid == 0) {
@@ -496,21 +497,23 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t heads, uint6
 
 size_t fwd_ts_item_bytes() { return sizeof(fwdts::Item); }
 
-// d in {64, 128}, ceil16(B) <= 128. item_off = exclusive scan of per-(head,
-// block) tile counts (128-row tiles), n_items its total (device).
+// item records for every (head, block): item_off = exclusive scan of the
+// per-(head, block) counts of 128-row tiles
+void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int32_t* item_off, int64_t total,
+                       void* items, cudaStream_t s) {
+    fwdts::fwd_ts_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, offsets, item_off, total,
+                                                                             (fwdts::Item*)items);
+}
+
+// d in {64, 128}, ceil16(B) <= 128; runs the items [*item_lo, *item_hi)
+// (device values) — a contiguous range of heads.
 template <int D>
 int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
-                  const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* item_off,
-                  void* items, const int32_t* n_items, int64_t max_items, float scale_log2, void* part_o,
-                  float* part_lse, cudaStream_t s) {
+                  const int32_t* flat, const void* items, const int32_t* item_lo, const int32_t* item_hi,
+                  float scale_log2, void* part_o, float* part_lse, cudaStream_t s) {
     using namespace fwdts;
     const int BP = (int)ceil_div(B, 16) * 16;
     if (BP > 128) return MOBA_ERR_UNSUPPORTED;
-    const int64_t total = bh * ceil_div(N, B);
-    fwd_ts_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, offsets, item_off, total,
-                                                                       (Item*)items);
-    int st = check_launch("fwd_ts_items_kernel");
-    if (st) return st;
     CUtensorMap tm_k, tm_v;
     if (!make_tmap_bf16_3d(&tm_k, k, (uint64_t)bh, (uint64_t)N, D, BP) ||
         !make_tmap_bf16_3d(&tm_v, v, (uint64_t)bh, (uint64_t)N, D, BP))
@@ -526,7 +529,7 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
               : nch == 3 ? moba_fwd_ts_kernel<D, 3>
                          : moba_fwd_ts_kernel<D, 4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs);
+    const int grid = kNumSMs;
     static long long* trace = nullptr;
     const char* trace_path = std::getenv("MOBA_FWD_TRACE");
     if (trace_path != nullptr && trace == nullptr) cudaMalloc(&trace, 256 * 16 * sizeof(long long));
@@ -534,10 +537,10 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
     {
         StageTimer tm(T_FWD, s);
         kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, flat,
-                                          (const Item*)items, n_items, scale_log2, (__nv_bfloat16*)part_o, part_lse, tm_po,
-                                          trace_path != nullptr ? trace : nullptr);
+                                          (const Item*)items, item_lo, item_hi, scale_log2, (__nv_bfloat16*)part_o,
+                                          part_lse, tm_po, trace_path != nullptr ? trace : nullptr);
     }
-    st = check_launch("moba_fwd_ts_kernel");
+    int st = check_launch("moba_fwd_ts_kernel");
     if (st == 0 && trace_path != nullptr) {
         static long long host[256 * 16];
         cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
@@ -551,10 +554,8 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
 }
 
 template int launch_fwd_ts<64>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,
-                               const int32_t*, const int32_t*, const int32_t*, void*, const int32_t*, int64_t, float,
-                               void*, float*, cudaStream_t);
+                               const void*, const int32_t*, const int32_t*, float, void*, float*, cudaStream_t);
 template int launch_fwd_ts<128>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,
-                                const int32_t*, const int32_t*, const int32_t*, void*, const int32_t*, int64_t, float,
-                                void*, float*, cudaStream_t);
+                                const void*, const int32_t*, const int32_t*, float, void*, float*, cudaStream_t);
 
 }  // namespace moba
