@@ -12,6 +12,7 @@
 // its query's running top-k list in registers.
 #include "common.cuh"
 #include "sm100.cuh"
+#include <cstdlib>
 
 namespace moba {
 
@@ -41,6 +42,27 @@ MOBA_DEV void topk_insert(float (&ts)[KMAX], int (&ti)[KMAX], float s, int j) {
 }
 
 
+// Insert a candidate whose block index is larger than every listed one (a
+// thread sees its candidates in ascending block order): it goes after every
+// entry with score >= s (equal scores keep the lower index first,
+// src/router.py:95-98). All slot tests read the old list, so the eight
+// compare/select groups are independent; s = -inf is a no-op.
+template <int KMAX>
+MOBA_DEV void topk_insert_tail(float (&ts)[KMAX], int (&ti)[KMAX], float s, int j) {
+    bool ge[KMAX];
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) ge[u] = ts[u] >= s;
+#pragma unroll
+    for (int u = KMAX - 1; u >= 1; --u) {
+        const float ns = ge[u - 1] ? s : ts[u - 1];
+        const int ni = ge[u - 1] ? j : ti[u - 1];
+        ts[u] = ge[u] ? ts[u] : ns;
+        ti[u] = ge[u] ? ti[u] : ni;
+    }
+    ts[0] = ge[0] ? ts[0] : s;
+    ti[0] = ge[0] ? ti[0] : j;
+}
+
 // Chunked, warp-friendly selection: each lane first compacts the candidates
 // of a 32-wide chunk that beat its (stale) threshold into a private smem
 // list with predicated stores, then the warp inserts them in lockstep. The
@@ -62,10 +84,9 @@ MOBA_DEV void select_chunk32(const float (&sv)[32], int j0, int lim, float (&ts)
     }
     const int iters = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
     for (int t = 0; t < iters; ++t) {
-        if (t < cnt) {
-            const float sc = buf_s[t * 33];
-            if (sc > ts[KMAX - 1]) topk_insert<KMAX>(ts, ti, sc, buf_i[t * 33]);
-        }
+        const float sc = buf_s[t * 33];
+        const int ix = buf_i[t * 33];
+        topk_insert_tail<KMAX>(ts, ti, (t < cnt && sc > ts[KMAX - 1]) ? sc : -INFINITY, ix);
     }
 }
 
@@ -355,6 +376,212 @@ route_topk_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
     for (int s2 = nvalid + 1; s2 < width; ++s2) row[s2] = -1;
 }
 
+// ---------------------------------------------------------------- tensor-core routing, 2 threads per query
+// Same scores and selection order as route_topk_tc_kernel, but 8 warps per
+// CTA: the two warps of a TMEM lane quadrant split each 64-centroid chunk
+// (columns 0-31 / 32-63), each keeps its own running top-k of the query,
+// and the two lists (disjoint block sets, both ordered by score desc /
+// index asc) are merged at the end. Candidates are compacted 16 at a time
+// (per-lane smem lists of 16), so two CTAs fit on an SM.
+constexpr int kRt2Threads = 256;
+constexpr int kRt2Buf = 16;
+
+template <int KMAX>
+MOBA_DEV void select_chunk16(const float* sv, int j0, int lim, float (&ts)[KMAX], int (&ti)[KMAX], float* buf_s,
+                             int* buf_i) {
+    const float thr = ts[KMAX - 1];
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (i < lim && sv[i] > thr) {
+            buf_s[cnt * 32] = sv[i];
+            buf_i[cnt * 32] = j0 + i;
+            ++cnt;
+        }
+    }
+    const int iters = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+    for (int t = 0; t < iters; ++t) {
+        const float sc = buf_s[t * 32];
+        const int ix = buf_i[t * 32];
+        topk_insert_tail<KMAX>(ts, ti, (t < cnt && sc > ts[KMAX - 1]) ? sc : -INFINITY, ix);
+    }
+}
+
+template <int D, int KMAX>
+__global__ void __launch_bounds__(kRt2Threads)
+route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
+                      int B, int top_k, int64_t split_rows, int32_t* __restrict__ topk) {
+    using namespace sm100;
+    constexpr int SL = D / 64;
+    constexpr uint32_t q_bytes = kRtM * D * 2;
+    constexpr uint32_t c_bytes = kRtN * D * 2;            // one split term of a chunk
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* q_s = smem;
+    uint8_t* c_s = q_s + q_bytes;                         // [2 buffers][3 terms][SL][64][128B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(c_s + 2 * 3 * c_bytes);   // tma[2], mma[2]
+    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 4);
+    float* sel_s = reinterpret_cast<float*>(tmem_ptr + 4);                   // [8 warps][16][32]
+    int* sel_i = reinterpret_cast<int*>(sel_s + 8 * kRt2Buf * 32);          // [8 warps][16][32]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int quad = warp & 3, half = warp >> 2;
+    const int64_t h = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * kRtM;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int width = top_k + 1;
+    const int64_t last_i = min64(r0 + kRtM, N) - 1;
+    const int max_own = (int)(last_i / B);
+    const int n_chunks = (max_own + kRtN - 1) / kRtN;
+
+    if (warp == 0) tmem_alloc(tmem_ptr, 2 * kRtN);
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_ptr;
+    const uint32_t idesc = idesc_bf16(kRtM, kRtN, false, false);
+
+    auto load_chunk = [&](int c, int buf) {   // thread 0
+        mbar_expect_tx(&bars[buf], 3 * c_bytes + (c == 0 ? q_bytes : 0));
+        if (c == 0) {
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+                tma_load_2d(smem_u32(q_s) + sl * kRtM * 128, &tm_q, sl * 64, (int)(h * N + r0), &bars[buf]);
+        }
+        const uint32_t cb = smem_u32(c_s) + buf * 3 * c_bytes;
+#pragma unroll
+        for (int term = 0; term < 3; ++term)
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+                tma_load_2d(cb + term * c_bytes + sl * kRtN * 128, &tm_c, sl * 64,
+                            (int)(term * split_rows + h * n_blocks + (int64_t)c * kRtN), &bars[buf]);
+    };
+    auto issue_mma = [&](int c) {             // thread 0
+        const int buf = c & 1;
+        mbar_wait(&bars[buf], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(q_s), cb = smem_u32(c_s) + buf * 3 * c_bytes;
+        bool acc = false;
+#pragma unroll
+        for (int term = 0; term < 3; ++term)
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const int sl = kk >> 2, ke = (kk & 3) * 16;
+                umma_bf16(tmem + buf * kRtN, desc_kmajor(qa + sl * kRtM * 128, ke),
+                          desc_kmajor(cb + term * c_bytes + sl * kRtN * 128, ke), idesc, acc);
+                acc = true;
+            }
+        umma_commit(&bars[2 + buf]);
+    };
+
+    if (tid == 0 && n_chunks > 0) {
+        load_chunk(0, 0);
+        if (n_chunks > 1) load_chunk(1, 1);
+        issue_mma(0);
+    }
+
+    const int row = 32 * quad + lane;
+    const int64_t my_i = r0 + row;
+    const int my_own = (int)(min64(my_i, N - 1) / B);
+    const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+    float* bs = sel_s + warp * kRt2Buf * 32 + lane;
+    int* bi = sel_i + warp * kRt2Buf * 32 + lane;
+    float ts[KMAX];
+    int ti[KMAX];
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        ts[u] = -INFINITY;
+        ti[u] = 0x7fffffff;
+    }
+    for (int c = 0; c < n_chunks; ++c) {
+        const int buf = c & 1;
+        mbar_wait(&bars[2 + buf], (c >> 1) & 1);        // S(c) in TMEM, smem buffer free
+        tc_fence_after();
+        if (tid == 0) {
+            if (c + 1 < n_chunks) issue_mma(c + 1);
+            if (c + 2 < n_chunks) load_chunk(c + 2, buf);
+        }
+        const int j0 = c * kRtN + 32 * half;
+        const int lim = (my_i < N) ? min(32, my_own - j0) : 0;   // strictly-past blocks only
+        if (!__all_sync(0xffffffffu, lim <= 0)) {
+            float sv[32];
+            tmem_ld32(tmem + buf * kRtN + 32 * half + lane_off, sv);
+            tmem_ld_wait();
+            select_chunk16<KMAX>(sv, j0, lim, ts, ti, bs, bi);
+            if (!__all_sync(0xffffffffu, lim <= 16)) select_chunk16<KMAX>(sv + 16, j0 + 16, lim - 16, ts, ti, bs, bi);
+        }
+        tc_fence_before();
+        __syncthreads();                                 // S buffer may be overwritten by MMA(c + 2)
+    }
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 2 * kRtN);
+    }
+    // merge the two halves' lists: half 1 publishes, half 0 merges and writes
+    float* ms = reinterpret_cast<float*>(c_s);                 // [KMAX][128] (C buffers are free now)
+    int* mi = reinterpret_cast<int*>(c_s + KMAX * kRtM * 4);
+    if (half == 1) {
+#pragma unroll
+        for (int u = 0; u < KMAX; ++u) {
+            ms[u * kRtM + row] = ts[u];
+            mi[u * kRtM + row] = ti[u];
+        }
+    }
+    __syncthreads();
+    if (half == 1 || my_i >= N) return;
+    int res[KMAX];
+    {
+        int a = 0, b = 0;
+        float bsc = ms[row];
+        int bix = mi[row];
+#pragma unroll
+        for (int u = 0; u < KMAX; ++u) {
+            float asc = -INFINITY;
+            int aix = 0x7fffffff;
+#pragma unroll
+            for (int v = 0; v < KMAX; ++v)
+                if (v == a) { asc = ts[v]; aix = ti[v]; }
+            const bool take_a = (asc > bsc) || (asc == bsc && aix < bix);
+            res[u] = take_a ? aix : bix;
+            if (take_a) {
+                ++a;
+            } else {
+                ++b;
+                bsc = (b < KMAX) ? ms[b * kRtM + row] : -INFINITY;
+                bix = (b < KMAX) ? mi[b * kRtM + row] : 0x7fffffff;
+            }
+        }
+    }
+    // keep the first top_k, sort the block ids ascending, append the own block
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u)
+        if (u >= top_k) res[u] = 0x7fffffff;
+#pragma unroll
+    for (int p = 0; p < KMAX; ++p) {
+#pragma unroll
+        for (int u = (p & 1); u + 1 < KMAX; u += 2) {
+            int x = res[u], y = res[u + 1];
+            res[u] = min(x, y);
+            res[u + 1] = max(x, y);
+        }
+    }
+    int32_t* out = topk + (h * N + my_i) * width;
+    int nvalid = 0;
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        if (res[u] != 0x7fffffff) {
+            out[u] = res[u];
+            ++nvalid;
+        }
+    }
+    out[nvalid] = my_own;
+    for (int s2 = nvalid + 1; s2 < width; ++s2) out[s2] = -1;
+}
+
 // ---------------------------------------------------------------- varlen
 // build_varlen as a stable counting sort over query chunks:
 //  count   : per (head, chunk of TQ queries) a shared-memory histogram over
@@ -396,23 +623,19 @@ varlen_scan_kernel(int32_t* __restrict__ cc, int n_blocks, int n_chunks, int32_t
     __shared__ int32_t carry;
     const int64_t h = blockIdx.x;
     int32_t* cch = cc + h * (int64_t)n_chunks * n_blocks;
-    // per block: exclusive scan over chunks
+    // per block: exclusive scan over chunks, 16 chunk loads in flight
     for (int b = threadIdx.x; b < n_blocks; b += blockDim.x) {
         int32_t run = 0;
         int c = 0;
-        for (; c + 4 <= n_chunks; c += 4) {
-            int32_t v0 = cch[(int64_t)(c + 0) * n_blocks + b];
-            int32_t v1 = cch[(int64_t)(c + 1) * n_blocks + b];
-            int32_t v2 = cch[(int64_t)(c + 2) * n_blocks + b];
-            int32_t v3 = cch[(int64_t)(c + 3) * n_blocks + b];
-            cch[(int64_t)(c + 0) * n_blocks + b] = run;
-            run += v0;
-            cch[(int64_t)(c + 1) * n_blocks + b] = run;
-            run += v1;
-            cch[(int64_t)(c + 2) * n_blocks + b] = run;
-            run += v2;
-            cch[(int64_t)(c + 3) * n_blocks + b] = run;
-            run += v3;
+        for (; c + 16 <= n_chunks; c += 16) {
+            int32_t v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = cch[(int64_t)(c + u) * n_blocks + b];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                cch[(int64_t)(c + u) * n_blocks + b] = run;
+                run += v[u];
+            }
         }
         for (; c < n_chunks; ++c) {
             int32_t v = cch[(int64_t)c * n_blocks + b];
@@ -455,50 +678,48 @@ varlen_scan_kernel(int32_t* __restrict__ cc, int n_blocks, int n_chunks, int32_t
     }
 }
 
-constexpr int kScatterBatch = 8;
-
-__global__ void __launch_bounds__(32)
+// The chunk's rows (TQ x width int32) are first staged in shared memory with
+// coalesced loads that are all in flight together; the ordered walk then
+// runs from shared memory.
+__global__ void __launch_bounds__(128)
 varlen_scatter_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int n_blocks, int TQ,
                       int n_chunks, const int32_t* __restrict__ cc, const int32_t* __restrict__ offsets,
                       int32_t* __restrict__ flat, int32_t* __restrict__ row_pos) {
-    extern __shared__ int32_t cursor[];
+    extern __shared__ int32_t vsm[];
+    int32_t* cursor = vsm;                   // [n_blocks]
+    int32_t* rows_s = vsm + n_blocks;        // [TQ * width]
     const int64_t h = blockIdx.y;
     const int chunk = blockIdx.x;
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x;
     const int32_t* ccc = cc + (h * n_chunks + chunk) * (int64_t)n_blocks;
-    for (int b = lane; b < n_blocks; b += 32) cursor[b] = offsets[h * n_blocks + b] + ccc[b];
-    __syncwarp();
     const int64_t i0 = (int64_t)chunk * TQ;
     const int64_t i1 = min64(i0 + TQ, N);
-    const int32_t* tk = topk + h * N * width;
-    int32_t* rp = row_pos + h * N * width;
+    const int nq = (int)(i1 - i0);
+    for (int b = tid; b < n_blocks; b += blockDim.x) cursor[b] = offsets[h * n_blocks + b] + ccc[b];
+    const int32_t* tk = topk + (h * N + i0) * width;
+    for (int e = tid; e < nq * width; e += blockDim.x) rows_s[e] = __ldg(tk + e);
+    __syncthreads();
+    int32_t* rp = row_pos + (h * N + i0) * width;
     int32_t* fl = flat + h * N * width;
-    // width <= 32: lane = slot, so one pass per query batch keeps the
-    // ascending-query order of every block's slice
-    for (int64_t ib = i0; ib < i1; ib += kScatterBatch) {
-        {
-            const int s = lane;
-            int32_t blk[kScatterBatch];
-#pragma unroll
-            for (int u = 0; u < kScatterBatch; ++u)
-                blk[u] = (ib + u < i1 && s < width) ? tk[(ib + u) * width + s] : -1;
-#pragma unroll
-            for (int u = 0; u < kScatterBatch; ++u) {
-                if (ib + u < i1) {
-                    int32_t b = blk[u];
-                    if (b >= 0) {
-                        int32_t p = cursor[b];
-                        cursor[b] = p + 1;
-                        fl[p] = (int32_t)(ib + u);
-                        rp[(ib + u) * width + s] = p;
-                    } else if (s < width) {
-                        rp[(ib + u) * width + s] = -1;
-                    }
-                }
-                __syncwarp();
+    if (tid < 32) {
+        // width <= 32: lane = slot; one query at a time keeps every block's
+        // slice in ascending query order (a row never repeats a block)
+        const int s = tid;
+        for (int q = 0; q < nq; ++q) {
+            const int32_t b = (s < width) ? rows_s[q * width + s] : -1;
+            if (b >= 0) {
+                const int32_t p = cursor[b];
+                cursor[b] = p + 1;
+                fl[p] = (int32_t)(i0 + q);
+                rows_s[q * width + s] = p;
+            } else if (s < width) {
+                rows_s[q * width + s] = -1;
             }
+            __syncwarp();
         }
     }
+    __syncthreads();
+    for (int e = tid; e < nq * width; e += blockDim.x) rp[e] = rows_s[e];
 }
 
 // row_pos from an arbitrary (validated) plan: binary search of query i in
@@ -614,10 +835,8 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     StageTimer tm(T_VARLEN, s);
     cudaMemsetAsync(err, 0, sizeof(int), s);
     size_t hsmem = (size_t)g.n_blocks * sizeof(int);
-    if (hsmem > 48 * 1024) {
+    if (hsmem > 48 * 1024)
         cudaFuncSetAttribute(varlen_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-        cudaFuncSetAttribute(varlen_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-    }
     varlen_count_kernel<<<dim3(g.n_chunks, (unsigned)bh), 256, hsmem, s>>>(topk, N, width, g.n_blocks, g.TQ,
                                                                         g.n_chunks, cc, err);
     int st = check_launch("varlen_count_kernel");
@@ -631,7 +850,12 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     varlen_scan_kernel<<<(unsigned)bh, 1024, 0, s>>>(cc, g.n_blocks, g.n_chunks, counts, offsets);
     st = check_launch("varlen_scan_kernel");
     if (st) return st;
-    varlen_scatter_kernel<<<dim3(g.n_chunks, (unsigned)bh), 32, hsmem, s>>>(
+    const size_t ssmem = hsmem + (size_t)g.TQ * width * sizeof(int32_t);
+    if (ssmem > 48 * 1024) {
+        if (ssmem > 227 * 1024) return MOBA_ERR_UNSUPPORTED;
+        cudaFuncSetAttribute(varlen_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+    }
+    varlen_scatter_kernel<<<dim3(g.n_chunks, (unsigned)bh), 128, ssmem, s>>>(
         topk, N, width, g.n_blocks, g.TQ, g.n_chunks, cc, offsets, flat, row_pos);
     return check_launch("varlen_scatter_kernel");
 }
@@ -651,11 +875,20 @@ static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N,
         if (!make_tmap_bf16(&tm_q, q, (uint64_t)(bh * N), D, kRtM) ||
             !make_tmap_bf16(&tm_c, split, (uint64_t)(3 * bh * n), D, kRtN))
             return MOBA_ERR_CUDA;
-        const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 4 * 33 * 33 * 4;
-        auto kern = route_topk_tc_kernel<D, KMAX>;
+        const char* impl = std::getenv("MOBA_ROUTE_IMPL");
+        if (impl != nullptr && impl[0] == '1') {
+            const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 4 * 33 * 33 * 4;
+            auto kern = route_topk_tc_kernel<D, KMAX>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh * n, topk);
+            return check_launch("route_topk_tc_kernel");
+        }
+        static_assert(2 * 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the C buffers");
+        const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
+        auto kern = route_topk_tc2_kernel<D, KMAX>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh * n, topk);
-        return check_launch("route_topk_tc_kernel");
+        kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh * n, topk);
+        return check_launch("route_topk_tc2_kernel");
     }
     const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
     cudaFuncSetAttribute(route_topk_fp32_kernel<D, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

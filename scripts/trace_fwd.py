@@ -16,11 +16,11 @@ torch.cuda.synchronize()
 t = np.fromfile(path, dtype=np.int64).reshape(256, 16)
 t0 = t[t > 0].min()
 names = ["mma:q_wait0", "mma:q_ok", "mma:p_wait0", "mma:p_ok", "pr:qe_wait0", "pr:qe_ok", "pr:issued",
-         "sm:s_wait0", "sm:s_ok", "sm:p_done", "sm:o_ok", "sm:epi_done", "mma:pv_iss", "mma:s_iss", "sm:o_ld"]
+         "sm:s_wait0", "sm:s_ok", "sm:p_done", "sm:o_ok", "sm:epi_done", "mma:pv_iss", "mma:s_iss", "sm:o_ld", "sm:s_free"]
 print("li  " + " ".join(f"{n:>11s}" for n in names))
 rows = [i for i in range(256) if t[i].any()]
 for i in rows[:int(os.environ.get("ROWS", 24))]:
-    print(f"{i:3d} " + " ".join(f"{(t[i, e] - t0) if t[i, e] else -1:11d}" for e in range(15)))
+    print(f"{i:3d} " + " ".join(f"{(t[i, e] - t0) if t[i, e] else -1:11d}" for e in range(16)))
 n = len(rows)
 span = t[rows].max() - t0
 print(f"items {n}, span {span} cycles, {span / max(n, 1):.0f} cycles/item")
