@@ -239,6 +239,46 @@ def run_ours(args, rank, world):
         clocks = sampler.summary(t_wall0, t_wall1)
 
     flops_rank = step_flops(H, N, d, B, k)
+    eager_ms = ms_max
+    eager_value = flops_rank * world * args.steps / (eager_ms / 1e3) / 1e12
+
+    # ---- the same step replayed as one CUDA graph (MobaGraphedStep: the
+    # public API for fixed-shape training loops); this is the headline value
+    graph_info = None
+    if not args.no_graph:
+        gs = mb.MobaGraphedStep((H, N, d), B, k, mode=args.route_mode, deterministic=args.deterministic)
+        gs.step(q, kk, v, do)
+        for _ in range(args.warmup):
+            gs.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        sampler_g = ClockSampler(dev.index) if rank == 0 else None
+        time.sleep(0.3 if sampler_g else 0)
+        tg0 = time.time()
+        for i in range(args.steps):
+            flush.zero_()
+            gevs[i][0].record()
+            gs.replay()
+            gevs[i][1].record()
+        torch.cuda.synchronize()
+        tg1 = time.time()
+        gms = torch.tensor([sum(a.elapsed_time(b) for a, b in gevs)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        if sampler_g:
+            time.sleep(0.25)
+            sampler_g.stop()
+            clocks = sampler_g.summary(tg0, tg1)
+        # parity of the replay against the eager step (same inputs)
+        out_e = mb.moba_attn(q, kk, v, B, k, mode=args.route_mode)
+        graph_info = {"ms_per_step": float(gms.item()) / args.steps,
+                      "launches_per_step": gs.launches_per_step,
+                      "max_abs_vs_eager_out": float((gs.out.float() - out_e.float()).abs().max().item())}
+        ms_max = float(gms.item())
+        launches = gs.launches_per_step * args.steps
+        del gs
     value = flops_rank * world * args.steps / (ms_max / 1e3) / 1e12
 
     # ---- end to end through the public host-buffer API: pinned host Q, K, V, dO
@@ -317,7 +357,11 @@ def run_ours(args, rank, world):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, seeded per rank)",
         "config": {"workload": f"configs[1]: {H} heads/GPU x N={N}, d={d}, B={B}, top-k {k}; step = centroids + "
-                               f"top-k routing ({args.route_mode}) + varlen + fwd + bwd",
+                               f"top-k routing ({args.route_mode}) + varlen + fwd + bwd"
+                               + (", replayed as one CUDA graph (MobaGraphedStep)" if graph_info else ", eager"),
+                   "submission": "cuda_graph" if graph_info else "eager",
+                   "eager": {"ms_per_step": eager_ms / args.steps, "value": eager_value},
+                   "graph": graph_info,
                    "heads_per_gpu": H, "seq_len": N, "head_dim": d, "block_size": B, "top_k": k,
                    "parallelism": f"heads sharded over {world} GPU(s), no collective",
                    "bwd_schedule": "deterministic" if args.deterministic else "parallel",
@@ -409,6 +453,7 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=4, help="head chunks of the host-buffer pipeline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="headline from eager launches instead of a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))

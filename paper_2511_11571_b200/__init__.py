@@ -24,6 +24,7 @@ from .router import CentroidMatrix, build_plan, build_varlen, compute_centroids,
 from .attention import AttentionOutput, MobaAttnFunction, moba_attention, moba_attn, moba_backward, moba_forward
 from .keyconv import ConvKernel, key_conv_backward, key_conv_forward, random_kernel
 from .pipeline import HostPipeline, moba_fwd_bwd_host
+from .graphs import MobaGraphedStep
 
 
 def validate_plan(plan, n_tokens: int, cfg: MobaConfig) -> None:

@@ -378,3 +378,21 @@ def test_host_pipeline_matches_device_path(n_chunks):
                          (dv_h, vg.grad, "dV")):
         assert not got.is_cuda
         assert torch.equal(got, ref.detach().cpu()), nm
+
+
+@pytest.mark.parametrize("conv", [False, True])
+def test_graphed_step_matches_eager(conv):
+    """MobaGraphedStep (the whole fwd+bwd captured once, replayed) gives
+    bitwise the eager results, also after the inputs change (a new plan)."""
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    H, N, d, B, k = 3, 1536, 64, 128, 4
+    w = (torch.rand(3, d, generator=gen, device="cuda") - 0.5) if conv else None
+    gs = mb.MobaGraphedStep((H, N, d), B, k, mode="tc", deterministic=True, conv_weight=w)
+    for trial in range(2):
+        q, kk, v, do = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(4))
+        out, dq, dk, dv = gs.step(q, kk, v, do)
+        qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
+        ref = mb.moba_attn(qg, kg, vg, B, k, mode="tc", deterministic=True, conv_weight=w)
+        ref.backward(do)
+        for got, exp, nm in ((out, ref, "O"), (dq, qg.grad, "dQ"), (dk, kg.grad, "dK"), (dv, vg.grad, "dV")):
+            assert torch.equal(got, exp), (trial, nm)
