@@ -27,6 +27,8 @@
 // item).
 #include "common.cuh"
 #include "sm100.cuh"
+#include <cstdio>
+#include <cstdlib>
 
 namespace moba {
 namespace bwdp {
@@ -111,8 +113,13 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                      int width, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                      const int32_t* __restrict__ flat, float scale, int n_items, int* __restrict__ sched,
                      float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
-                     __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV) {
+                     __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, long long* __restrict__ trace) {
     using namespace sm100;
+    // debug timeline (MOBA_BWD_TRACE): CTA 0, lane 0 of the recording warp, per tile g
+#define TRB(g, ev)                                                                          \
+    do {                                                                                    \
+        if (trace != nullptr && blockIdx.x == 0 && lane == 0 && (g) < 256) trace[(g) * 16 + (ev)] = clock64(); \
+    } while (0)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -216,7 +223,9 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                     lv[i] = (qv[i] >= 0) ? lse[x.h * N + qv[i]] * kLog2e : 0.f;
                     dv[i] = (qv[i] >= 0) ? Dd[x.h * N + qv[i]] : 0.f;
                 }
+                if (warp == 0) TRB(g, 0);
                 mbar_wait(&bars->qd_empty[st], ((g / kQSt) & 1) ^ 1);
+                if (warp == 0) TRB(g, 1);
                 const uint32_t qb = qd_addr(st), db = qb + kTile;
 #pragma unroll
                 for (int i = 0; i < NI; ++i) {
@@ -239,6 +248,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                     }
                 }
                 mbar_arrive(&bars->qd_full[st]);
+                if (warp == 0) TRB(g, 2);
             }
         }
     } else if (warp == kMma) {
@@ -271,6 +281,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
             if (tl.first) mbar_wait(&bars->kv_full[tl.kvs], (tl.kvu >> 1) & 1);
             mbar_wait(&bars->qd_full[g % kQSt], (g / kQSt) & 1);
             mbar_wait(&bars->dq_empty[g & 1], ((g >> 1) & 1) ^ 1);
+            TRB(g, 3);
             tc_fence_after();
             fence_proxy_async_smem();
             if (lane == 0) {
@@ -305,6 +316,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
             if (have_n) issue_s(nxt, g + 1);
             mbar_wait(&bars->p_full, g & 1);
             if (cur.first) mbar_wait(&bars->dkv_empty, (cur.kvu & 1) ^ 1);
+            TRB(g, 4);
             tc_fence_after();
             fence_proxy_async_smem();
             if (lane == 0) {
@@ -328,6 +340,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 }
             }
             __syncwarp();
+            TRB(g, 5);
             if (have_n) issue_dp(nxt, g + 1);
             cur = nxt;
             have = have_n;
@@ -353,7 +366,9 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 const uint32_t la = ldi_addr(st), da = la + 512, ia = la + 1024;
                 const uint32_t slot = tmem + cS0 + (g & 1) * 128;
                 const int rows_t = min(MQ, x.cnt - t * MQ);
+                if (warp == kSm0) TRB(g, 6);
                 mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
+                if (warp == kSm0) TRB(g, 7);
                 tc_fence_after();
                 // slices ascend: a tile whose first query is at or past the
                 // slab's last key needs no causal mask
@@ -386,8 +401,10 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
                 named_bar(1 + quad, 64);        // both halves have read S^T from the slot
                 tmem_st32(slot + lane_off + 32 * half, pk);
+                if (warp == kSm0) TRB(g, 8);
                 // ---- phase B
                 mbar_wait(&bars->dp_full, g & 1);
+                if (warp == kSm0) TRB(g, 9);
                 tc_fence_after();
                 uint32_t dk[32];
 #pragma unroll
@@ -417,6 +434,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full);
+                if (warp == kSm0) TRB(g, 10);
             }
         }
     } else {
@@ -434,6 +452,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
             for (int t = 0; t < x.n_tiles; ++t, ++g) {
                 const int st = g % kQSt;
                 mbar_wait(&bars->dq_full[g & 1], (g >> 1) & 1);
+                if (warp == kEp0) TRB(g, 11);
                 tc_fence_after();
                 const int qi = lds32i(ldi_addr(st) + 1024 + row * 4);
                 __syncwarp();
@@ -530,10 +549,25 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
     auto kern = moba_bwd_pipe_kernel;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     const int grid = (int)std::min<int64_t>(n_items, kNumSMs);
+    static long long* trace = nullptr;
+    const char* trace_path = std::getenv("MOBA_BWD_TRACE");
+    if (trace_path != nullptr && trace == nullptr) cudaMalloc(&trace, 256 * 16 * sizeof(long long));
+    if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
     kern<<<grid, kThreads, kSmem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, bh,
                                        N, B, width, counts, offsets, flat, scale, (int)n_items, sched, dq_acc, dq_part,
-                                       part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
-    return check_launch("moba_bwd_pipe_kernel");
+                                       part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
+                                       trace_path != nullptr ? trace : nullptr);
+    int st = check_launch("moba_bwd_pipe_kernel");
+    if (st == 0 && trace_path != nullptr) {
+        static long long host[256 * 16];
+        cudaMemcpyAsync(host, trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            std::fwrite(host, sizeof(host), 1, f);
+            std::fclose(f);
+        }
+    }
+    return st;
 }
 
 }  // namespace moba
