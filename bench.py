@@ -372,7 +372,7 @@ def run_ours(args, rank, world):
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": float(te.item()) / args.steps,
                 "path": f"pinned host Q,K,V,dO -> moba_fwd_bwd_host (public API; {args.e2e_chunks} head chunks, "
-                        f"H2D / kernels / D2H on 3 streams) -> host O,LSE,dQ,dK,dV"},
+                        f"H2D / one CUDA-graph replay per chunk / D2H on 3 streams) -> host O,LSE,dQ,dK,dV"},
         "gpu_launches": launches,
         "clocks": clocks,
         "extra": extra,

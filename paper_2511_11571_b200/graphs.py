@@ -47,7 +47,7 @@ class MobaGraphedStep:
         n0 = lib.moba_launch_count()
         self._zero_grads()
         with torch.cuda.graph(self.graph):
-            self.out = self._body()
+            self.out, self.lse = self._body()
         self.launches_per_step = int(lib.moba_launch_count() - n0)
 
     def _zero_grads(self):
@@ -57,14 +57,19 @@ class MobaGraphedStep:
 
     def _body(self):
         self._zero_grads()
-        out = moba_attn(self.q, self.k, self.v, self.block_size, self.top_k, conv_weight=self.conv_weight,
-                        mode=self.mode, deterministic=self.deterministic)
+        out, lse = moba_attn(self.q, self.k, self.v, self.block_size, self.top_k, conv_weight=self.conv_weight,
+                             mode=self.mode, deterministic=self.deterministic, return_lse=True)
         out.backward(self.dout)
-        return out
+        return out, lse
 
     def replay(self):
-        """Re-run the captured step on the current contents of the static buffers."""
+        """Re-run the captured step on the current contents of the static
+        buffers (on the current stream)."""
         self.graph.replay()
+
+    @property
+    def grads(self):
+        return self.q.grad, self.k.grad, self.v.grad
 
     def step(self, q=None, k=None, v=None, dout=None):
         """Copy new inputs (device tensors of the captured shape) and replay.

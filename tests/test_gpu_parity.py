@@ -361,8 +361,9 @@ def test_routing_tensor_core_mode_c2_scale():
         assert not bad, (h, bad[:5], nd)
 
 
+@pytest.mark.parametrize("graphs", [False, True])
 @pytest.mark.parametrize("n_chunks", [1, 3])
-def test_host_pipeline_matches_device_path(n_chunks):
+def test_host_pipeline_matches_device_path(n_chunks, graphs):
     """moba_fwd_bwd_host (pinned host buffers, chunked over heads, copies on
     their own streams) returns bitwise the device path's results."""
     gen = torch.Generator(device="cuda").manual_seed(11)
@@ -372,8 +373,9 @@ def test_host_pipeline_matches_device_path(n_chunks):
     out, lse = mb.moba_attn(qg, kg, vg, B, k, mode="tc", deterministic=True, return_lse=True)
     out.backward(do)
     host = [t.cpu().pin_memory() for t in (q, kk, v, do)]
-    o_h, lse_h, dq_h, dk_h, dv_h = mb.moba_fwd_bwd_host(*host, B, k, n_chunks=n_chunks, mode="tc",
-                                                        deterministic=True)
+    for _ in range(2):   # the second call reuses the captured chunk graphs
+        o_h, lse_h, dq_h, dk_h, dv_h = mb.moba_fwd_bwd_host(*host, B, k, n_chunks=n_chunks, mode="tc",
+                                                            deterministic=True, graphs=graphs)
     for got, ref, nm in ((o_h, out, "O"), (lse_h, lse, "LSE"), (dq_h, qg.grad, "dQ"), (dk_h, kg.grad, "dK"),
                          (dv_h, vg.grad, "dV")):
         assert not got.is_cuda
