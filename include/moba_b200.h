@@ -174,6 +174,32 @@ int moba_bwd(const void* q, const void* k, const void* v,
              void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * Grouped-query attention (GQA / MQA). Same operations as
+ * moba_route / moba_fwd / moba_bwd with `bh` QUERY heads sharing
+ * bh / kv_group K/V heads: query head h reads K, V (and, for routing, the
+ * centroids) of K/V head h / kv_group. centroids, k, v, dk, dv are
+ * [bh / kv_group, n_tokens, head_dim]; dK / dV are the sums over the
+ * kv_group query heads of each K/V head (fixed order). kv_group = 1 is the
+ * reference's multi-head case (the plain entry points call these).
+ */
+int moba_route_gqa(const void* q, const float* centroids, int64_t bh, int kv_group,
+                   int64_t n_tokens, int head_dim, int block_size, int top_k, int mode,
+                   int32_t* topk, int32_t* counts, int32_t* offsets, int32_t* flat, int32_t* row_pos,
+                   void* workspace, size_t workspace_bytes, void* stream);
+int moba_fwd_gqa(const void* q, const void* k, const void* v, int64_t bh, int kv_group,
+                 int64_t n_tokens, int head_dim, int block_size, int width,
+                 const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* row_pos,
+                 float softmax_scale, void* out, float* lse,
+                 void* workspace, size_t workspace_bytes, void* stream);
+size_t moba_bwd_gqa_workspace_size(int64_t bh, int kv_group, int64_t n_tokens, int head_dim,
+                                   int block_size, int width, int deterministic);
+int moba_bwd_gqa(const void* q, const void* k, const void* v, const void* out, const void* dout,
+                 const float* lse, int64_t bh, int kv_group, int64_t n_tokens, int head_dim,
+                 int block_size, int width, const int32_t* counts, const int32_t* offsets,
+                 const int32_t* flat, const int32_t* row_pos, int deterministic, float softmax_scale,
+                 void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Key-conv backward (key_conv_backward, src/keyconv.py:81-104):
  *   g = dK' * silu'(a);  dK = dK' + sum_l W[l] * g_{t+l};  dW[l] = sum_t g_t K_{t-l}
  * k, dk_conv: bf16 [bh, n_tokens, head_dim]; dk: bf16 out; dw: fp32

@@ -65,19 +65,30 @@ def _empty_plan(H, N, width, n, device):
             torch.empty((H, N * width), **i32), torch.empty((H, N, width), **i32))
 
 
+def kv_group_of(q: torch.Tensor, kv: torch.Tensor) -> int:
+    """Query heads per K/V head (GQA/MQA; 1 = MHA)."""
+    Hq, Hk = q.shape[0], kv.shape[0]
+    if Hk < 1 or Hq % Hk != 0:
+        raise ShapeError(f"{Hq} query heads are not a multiple of {Hk} key/value heads")
+    return Hq // Hk
+
+
 def route(q: torch.Tensor, cent: torch.Tensor, block_size: int, top_k: int, mode: int = _lib.MOBA_ROUTE_FP32):
+    """Routing plan per QUERY head; `cent` may have fewer (K/V) heads (GQA:
+    query head h routes against the centroids of K/V head h // group)."""
     lib = _lib.load()
     H, N, Dp = q.shape
+    G = kv_group_of(q, cent)
     if top_k > MAX_TOP_K:
         raise ConfigError(f"top_k={top_k} > {MAX_TOP_K} is not supported by the compiled kernels")
     n = cent.shape[1]
     width = top_k + 1
     topk, counts, offsets, flat, row_pos = _empty_plan(H, N, width, n, q.device)
     ws = _ws(lib.moba_route_workspace_size(H, N, block_size, top_k), q.device)
-    st = lib.moba_route(q.data_ptr(), cent.data_ptr(), H, N, Dp, block_size, top_k, mode,
+    st = lib.moba_route_gqa(q.data_ptr(), cent.data_ptr(), H, G, N, Dp, block_size, top_k, mode,
                         topk.data_ptr(), counts.data_ptr(), offsets.data_ptr(), flat.data_ptr(),
                         row_pos.data_ptr(), ws.data_ptr(), ws.numel(), _stream(q))
-    _lib.check(st, "moba_route")
+    _lib.check(st, "moba_route_gqa")
     return RoutingPlan(topk, counts, offsets, flat, row_pos, N, block_size)
 
 
@@ -135,14 +146,15 @@ def fwd(q, k, v, plan: RoutingPlan, scale: float):
     if B > MAX_BLOCK:
         raise ConfigError(f"block_size={B} > {MAX_BLOCK} is not supported by the compiled kernels")
     ensure_row_pos(plan)
+    G = kv_group_of(q, k)
     out = torch.empty_like(q)
     lse = torch.empty((H, N), dtype=torch.float32, device=q.device)
     ws = _ws(lib.moba_fwd_workspace_size(H, N, Dp, B, plan.width), q.device)
-    st = lib.moba_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), H, N, Dp, B, plan.width,
+    st = lib.moba_fwd_gqa(q.data_ptr(), k.data_ptr(), v.data_ptr(), H, G, N, Dp, B, plan.width,
                       plan.counts_d.data_ptr(), plan.offsets_d.data_ptr(), plan.flat_d.data_ptr(),
                       plan.row_pos.data_ptr(), float(scale), out.data_ptr(), lse.data_ptr(),
                       ws.data_ptr(), ws.numel(), _stream(q))
-    _lib.check(st, "moba_fwd")
+    _lib.check(st, "moba_fwd_gqa")
     return out, lse
 
 
@@ -152,16 +164,17 @@ def bwd(q, k, v, out, dout, lse, plan: RoutingPlan, scale: float, deterministic:
     B = plan.block_size
     if deterministic:
         ensure_row_pos(plan)
+    G = kv_group_of(q, k)
     dq = torch.empty_like(q)
     dk = torch.empty_like(k)
     dv = torch.empty_like(v)
-    ws = _ws(lib.moba_bwd_workspace_size(H, N, Dp, B, plan.width, int(deterministic)), q.device)
-    st = lib.moba_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), dout.data_ptr(),
-                      lse.data_ptr(), H, N, Dp, B, plan.width, plan.counts_d.data_ptr(),
+    ws = _ws(lib.moba_bwd_gqa_workspace_size(H, G, N, Dp, B, plan.width, int(deterministic)), q.device)
+    st = lib.moba_bwd_gqa(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), dout.data_ptr(),
+                      lse.data_ptr(), H, G, N, Dp, B, plan.width, plan.counts_d.data_ptr(),
                       plan.offsets_d.data_ptr(), plan.flat_d.data_ptr(),
                       _lib.ptr(plan.row_pos) if deterministic else None, int(deterministic), float(scale),
                       dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(), _stream(q))
-    _lib.check(st, "moba_bwd")
+    _lib.check(st, "moba_bwd_gqa")
     return dq, dk, dv
 
 

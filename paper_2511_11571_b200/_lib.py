@@ -48,6 +48,12 @@ SIGNATURES = {
     "moba_fwd": (_i32, [_p, _p, _p, _i64, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _f32, _p, _p, _p, _sz, _p]),
     "moba_bwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _i32,
                         _f32, _p, _p, _p, _p, _sz, _p]),
+    "moba_route_gqa": (_i32, [_p, _p, _i64, _i32, _i64, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "moba_fwd_gqa": (_i32, [_p, _p, _p, _i64, _i32, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _f32, _p, _p, _p, _sz,
+                            _p]),
+    "moba_bwd_gqa_workspace_size": (_sz, [_i64, _i32, _i64, _i32, _i32, _i32, _i32]),
+    "moba_bwd_gqa": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _i32,
+                            _f32, _p, _p, _p, _p, _sz, _p]),
     "moba_conv_bwd_workspace_size": (_sz, [_i64, _i64, _i32, _i32]),
     "moba_conv_bwd": (_i32, [_p, _p, _i32, _p, _i64, _i64, _i32, _p, _p, _p, _sz, _p]),
     "moba_launch_count": (ctypes.c_ulonglong, []),

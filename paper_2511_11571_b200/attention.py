@@ -162,10 +162,27 @@ class MobaAttnFunction(torch.autograd.Function):
         return dq, dk, dv, dw, None, None, None, None, None
 
 
+def _check_gqa(q, k, v):
+    """q [..., Hq, N, d]; k, v [..., Hkv, N, d] with Hq a multiple of Hkv
+    (GQA; Hkv = 1 is MQA; Hkv = Hq is the reference's MHA)."""
+    if tuple(k.shape) != tuple(v.shape):
+        raise ShapeError(f"k{tuple(k.shape)} and v{tuple(v.shape)} must match")
+    if q.dim() < 2 or k.dim() != q.dim():
+        raise ShapeError(f"q{tuple(q.shape)} and k{tuple(k.shape)} must have the same rank (>= 2)")
+    if tuple(k.shape) == tuple(q.shape):
+        return
+    if q.dim() < 3 or q.shape[:-3] != k.shape[:-3] or q.shape[-2:] != k.shape[-2:] or q.shape[-3] % k.shape[-3]:
+        raise ShapeError(f"GQA needs q[..., Hq, N, d] and k/v[..., Hkv, N, d] with Hkv dividing Hq, "
+                         f"got q{tuple(q.shape)} k{tuple(k.shape)}")
+
+
 def moba_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_size: int, top_k: int,
               causal: bool = True, conv_weight: torch.Tensor | None = None, mode: str = "fp32",
               deterministic: bool = False, return_lse: bool = False):
     """Batched MoBA attention for bf16 CUDA tensors [..., N, d] (d <= 128).
+    k and v may have fewer heads than q (GQA/MQA, [..., Hkv, N, d]): query
+    head h uses K/V head h // (Hq / Hkv) for routing and attention, and dK /
+    dV are summed over the query heads sharing a K/V head.
 
     The north-star facade (q, k, v, block size B, top-k, causal). Only causal
     attention exists in the reference (src/attention.py:127-133), so
@@ -176,7 +193,7 @@ def moba_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_size: int
         raise ConfigError("MoBA attention is causal only (src/attention.py:127-133)")
     MobaConfig(block_size_B=block_size, top_k=top_k, head_dim_d=q.shape[-1],
                conv_width=0 if conv_weight is None else int(conv_weight.shape[0]))
-    _check_qkv(q, k, v)
+    _check_gqa(q, k, v)
     for name, t in (("q", q), ("k", k), ("v", v)):
         _device.require_cuda(t, name)
     lead, N, d = tuple(q.shape[:-2]), q.shape[-2], q.shape[-1]
@@ -192,6 +209,8 @@ def moba_attn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_size: int
         if dp != d:
             w = torch.nn.functional.pad(w, (0, dp - d))
         w = w.contiguous()
+    # GQA / MQA: k, v flatten to [batch * Hkv, N, d]; flat query head i maps
+    # to flat K/V head i // (Hq / Hkv) (batch-major flattening keeps that exact)
     out, lse = MobaAttnFunction.apply(kern(q), kern(k), kern(v), w, block_size, top_k,
                                       _device.softmax_scale(d), ROUTE_MODES[mode], deterministic)
     out = out[..., :d].reshape(*lead, N, d)

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kBwdTcThreads, 1)
 moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ dO,
                    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const float* __restrict__ lse, const float* __restrict__ Dd, int64_t N, int B, int width,
-                   const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                   int kv_group, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                    const int32_t* __restrict__ flat, float scale, int qstages, int64_t n_items,
                    float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
                    __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV) {
@@ -354,7 +354,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 mbar_wait(&bars->kv_empty, (kv_use & 1) ^ 1);
                 if (lane == 0) {
                     mbar_expect_tx(&bars->kv_full, 2 * kv_bytes);
-                    const int row0 = (int)(h * N + kb0);
+                    const int row0 = (int)((h / kv_group) * N + kb0);   // GQA: K/V head of query head h
 #pragma unroll
                     for (int sl = 0; sl < D / 64; ++sl) {
                         tma_load_2d(smem_u32(k_s) + sl * KT * 128, &tm_k, sl * 64, row0, &bars->kv_full);
@@ -724,17 +724,40 @@ __global__ void bwd_dq_combine_kernel(const float* __restrict__ dq_part, int64_t
 }
 
 int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* Dd,
-                    int64_t bh, int64_t N, int B, int width, const int32_t* counts, const int32_t* offsets,
+                    int64_t bh, int kv_group, int64_t N, int B, int width, const int32_t* counts, const int32_t* offsets,
                     const int32_t* flat, float scale, int* sched, float* dq_acc, float* dq_part,
                     int64_t part_stride, void* dk, void* dv, cudaStream_t s);
 
 // workspace: sched int (256 B) | Dd f32 [bh*N] | dq_acc f32 [bh*N*D] |
 // (deterministic) dq_part f32 [slabs][bh*N*width*D]
 static int bwd_kt(int B) { return B > 64 ? 128 : 64; }
-static size_t bwd_ws(int64_t bh, int64_t N, int D, int B, int width, bool det) {
+static size_t bwd_ws(int64_t bh, int64_t N, int D, int B, int width, bool det, int kv_group = 1) {
     size_t w = 256 + align_up((size_t)bh * N * 4, 256) + align_up((size_t)bh * N * D * 4, 256);
     if (det) w += (size_t)ceil_div(B, bwd_kt(B)) * bh * N * width * D * 4;
+    if (kv_group > 1) w += 2 * align_up((size_t)bh * N * D * 2, 256);   // per-query-head dK, dV (bf16)
     return w;
+}
+
+// GQA: dK/dV of a K/V head = sum over its kv_group query heads (fp32 sum of
+// the per-query-head bf16 gradients, fixed order -> deterministic)
+__global__ void gqa_group_sum_kernel(const __nv_bfloat16* __restrict__ src, int64_t kv_rows_elems, int64_t head_elems,
+                                     int kv_group, __nv_bfloat16* __restrict__ dst) {
+    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (e >= kv_rows_elems) return;
+    const int64_t hk = e / head_elems, off = e - hk * head_elems;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int g = 0; g < kv_group; ++g) {
+        const uint4 u = *reinterpret_cast<const uint4*>(src + (hk * kv_group + g) * head_elems + off);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float2 f = unpack_bf16(w[c]);
+            acc[2 * c] += f.x;
+            acc[2 * c + 1] += f.y;
+        }
+    }
+    *reinterpret_cast<uint4*>(dst + e) = make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]),
+                                                    pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
 }
 
 template <int D, int KT>
@@ -756,9 +779,9 @@ static int launch_bwd_main(const void* q, const void* k, const void* v, const vo
 
 template <int D>
 static int launch_bwd(const void* q, const void* k, const void* v, const void* out, const void* dout,
-                      const float* lse, int64_t bh, int64_t N, int B, int width, const int32_t* counts,
+                      const float* lse, int64_t bh, int kv_group, int64_t N, int B, int width, const int32_t* counts,
                       const int32_t* offsets, const int32_t* flat, const int32_t* row_pos, bool det, float scale,
-                      void* dq, void* dk, void* dv, uint8_t* ws, cudaStream_t s) {
+                      void* dq, void* dk_out, void* dv_out, uint8_t* ws, cudaStream_t s) {
     int* sched = (int*)ws;
     ws += 256;
     float* Dd = (float*)ws;
@@ -767,6 +790,15 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     const int64_t part_stride = bh * N * width * D;
     const int slabs = (int)ceil_div(B, bwd_kt(B));
     const int64_t rows = bh * N;
+    // GQA: the kernels write per-query-head dK / dV, summed per group below
+    void* dk = dk_out;
+    void* dv = dv_out;
+    if (kv_group > 1) {
+        uint8_t* g = (uint8_t*)dq_acc + align_up((size_t)bh * N * D * 4, 256) +
+                     (det ? (size_t)slabs * bh * N * width * D * 4 : 0);
+        dk = g;
+        dv = g + align_up((size_t)bh * N * D * 2, 256);
+    }
     {
     StageTimer tm(T_BWD_PRE, s);
     bwd_preprocess_kernel<D><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>((const __nv_bfloat16*)out,
@@ -781,9 +813,10 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if (D == 64 && !(impl != nullptr && (impl[0] == 'm' || impl[0] == 't'))) {
         // pipelined tcgen05 kernel (attn_bwd_pipe.cu); dq_part slabs follow its 128-key slabs
         (void)slabs_tc;
-        st = launch_bwd_pipe(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale, sched, dq_acc,
-                             dq_part, part_stride, dk, dv, s);
+        st = launch_bwd_pipe(q, k, v, dout, lse, Dd, bh, kv_group, N, B, width, counts, offsets, flat, scale, sched,
+                             dq_acc, dq_part, part_stride, dk, dv, s);
     } else if (impl != nullptr && impl[0] == 'm') {
+        if (kv_group > 1) return MOBA_ERR_UNSUPPORTED;   // legacy mma.sync kernel: MHA only
         if (B > 64)
             st = launch_bwd_main<D, 128>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
                                          dq_acc, dq_part, part_stride, dk, dv, s);
@@ -808,20 +841,30 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
             g_last_trace = trp;
         }
         CUtensorMap tm_k, tm_v;
-        if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh * N), D, 128) || !make_tmap_bf16(&tm_v, v, (uint64_t)(bh * N), D, 128))
+        if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh / kv_group * N), D, 128) ||
+            !make_tmap_bf16(&tm_v, v, (uint64_t)(bh / kv_group * N), D, 128))
             return MOBA_ERR_CUDA;
         auto kern = moba_bwd_tc_kernel<D>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t n_items = bh * ceil_div(N, B) * ceil_div(B, 128);
         const int grid = (int)std::min<int64_t>(n_items, kNumSMs);
         kern<<<grid, kBwdTcThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, N, B,
-                                               width, counts, offsets, flat, scale, qstages, n_items, dq_acc,
+                                               width, kv_group, counts, offsets, flat, scale, qstages, n_items, dq_acc,
                                                dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
         st = check_launch("moba_bwd_tc_kernel");
     }
     }
     if (st) return st;
     StageTimer tm(T_BWD_POST, s);
+    if (kv_group > 1) {
+        const int64_t kv_elems = bh / kv_group * N * D;
+        for (int which = 0; which < 2; ++which)
+            gqa_group_sum_kernel<<<(unsigned)ceil_div(kv_elems / 8, 256), 256, 0, s>>>(
+                (const __nv_bfloat16*)(which ? dv : dk), kv_elems, N * D, kv_group,
+                (__nv_bfloat16*)(which ? dv_out : dk_out));
+        st = check_launch("gqa_group_sum_kernel", 2);
+        if (st) return st;
+    }
     if (det) {
         bwd_dq_combine_kernel<D><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(dq_part, part_stride, slabs, row_pos, N,
                                                                            width, rows, scale, (__nv_bfloat16*)dq);
@@ -836,10 +879,37 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
 
 using namespace moba;
 
+extern "C" size_t moba_bwd_gqa_workspace_size(int64_t bh, int kv_group, int64_t n_tokens, int head_dim,
+                                              int block_size, int width, int deterministic) {
+    if (bh < 1 || n_tokens < 1 || block_size < 1 || width < 1 || kv_group < 1) return 0;
+    return bwd_ws(bh, n_tokens, head_dim, block_size, width, deterministic != 0, kv_group);
+}
+
 extern "C" size_t moba_bwd_workspace_size(int64_t bh, int64_t n_tokens, int head_dim, int block_size, int width,
                                           int deterministic) {
-    if (bh < 1 || n_tokens < 1 || block_size < 1 || width < 1) return 0;
-    return bwd_ws(bh, n_tokens, head_dim, block_size, width, deterministic != 0);
+    return moba_bwd_gqa_workspace_size(bh, 1, n_tokens, head_dim, block_size, width, deterministic);
+}
+
+extern "C" int moba_bwd_gqa(const void* q, const void* k, const void* v, const void* out, const void* dout,
+                            const float* lse, int64_t bh, int kv_group, int64_t n_tokens, int head_dim, int block_size,
+                            int width, const int32_t* counts, const int32_t* offsets, const int32_t* flat,
+                            const int32_t* row_pos, int deterministic, float softmax_scale, void* dq, void* dk,
+                            void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+    if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
+    if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
+    if (block_size > 256 || width > 32) return MOBA_ERR_UNSUPPORTED;
+    const bool det = deterministic != 0;
+    if (det && row_pos == nullptr) return MOBA_ERR_PLAN;
+    if (workspace_bytes < bwd_ws(bh, n_tokens, head_dim, block_size, width, det, kv_group)) return MOBA_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = (uint8_t*)workspace;
+    if (head_dim == 64)
+        return launch_bwd<64>(q, k, v, out, dout, lse, bh, kv_group, n_tokens, block_size, width, counts, offsets,
+                              flat, row_pos, det, softmax_scale, dq, dk, dv, ws, s);
+    if (head_dim == 128)
+        return launch_bwd<128>(q, k, v, out, dout, lse, bh, kv_group, n_tokens, block_size, width, counts, offsets,
+                               flat, row_pos, det, softmax_scale, dq, dk, dv, ws, s);
+    return MOBA_ERR_UNSUPPORTED;
 }
 
 extern "C" int moba_bwd(const void* q, const void* k, const void* v, const void* out, const void* dout,
@@ -847,20 +917,8 @@ extern "C" int moba_bwd(const void* q, const void* k, const void* v, const void*
                         const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* row_pos,
                         int deterministic, float softmax_scale, void* dq, void* dk, void* dv, void* workspace,
                         size_t workspace_bytes, void* stream) {
-    if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
-    if (block_size > 256 || width > 32) return MOBA_ERR_UNSUPPORTED;
-    const bool det = deterministic != 0;
-    if (det && row_pos == nullptr) return MOBA_ERR_PLAN;
-    if (workspace_bytes < bwd_ws(bh, n_tokens, head_dim, block_size, width, det)) return MOBA_ERR_WORKSPACE;
-    cudaStream_t s = (cudaStream_t)stream;
-    uint8_t* ws = (uint8_t*)workspace;
-    if (head_dim == 64)
-        return launch_bwd<64>(q, k, v, out, dout, lse, bh, n_tokens, block_size, width, counts, offsets, flat,
-                              row_pos, det, softmax_scale, dq, dk, dv, ws, s);
-    if (head_dim == 128)
-        return launch_bwd<128>(q, k, v, out, dout, lse, bh, n_tokens, block_size, width, counts, offsets, flat,
-                               row_pos, det, softmax_scale, dq, dk, dv, ws, s);
-    return MOBA_ERR_UNSUPPORTED;
+    return moba_bwd_gqa(q, k, v, out, dout, lse, bh, 1, n_tokens, head_dim, block_size, width, counts, offsets, flat,
+                        row_pos, deterministic, softmax_scale, dq, dk, dv, workspace, workspace_bytes, stream);
 }
 
 extern "C" int moba_debug_trace(long long* host, int n) {

@@ -109,8 +109,8 @@ struct RingReader {
 __global__ void __launch_bounds__(kThreads, 1)
 moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ dO,
                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                     const float* __restrict__ lse, const float* __restrict__ Dd, int64_t bh, int64_t N, int B,
-                     int width, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                     const float* __restrict__ lse, const float* __restrict__ Dd, int64_t bh, int kv_group, int64_t N,
+                     int B, int width, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                      const int32_t* __restrict__ flat, float scale, int n_items, int* __restrict__ sched,
                      float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
                      __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, long long* __restrict__ trace) {
@@ -192,7 +192,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 mbar_wait(&bars->kv_empty[ks], ((kv_use >> 1) & 1) ^ 1);
                 if (lane == 0) {
                     mbar_expect_tx(&bars->kv_full[ks], 2 * kTile);
-                    const int row0 = (int)(x.h * N + x.kb0);
+                    const int row0 = (int)((x.h / kv_group) * N + x.kb0);   // GQA: K/V head of query head x.h
                     tma_load_2d(kv_addr(ks), &tm_k, 0, row0, &bars->kv_full[ks]);
                     tma_load_2d(kv_addr(ks) + kTile, &tm_v, 0, row0, &bars->kv_full[ks]);
                 }
@@ -535,13 +535,14 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
 
 // host launcher (attn_bwd.cu): d = 64, block_size <= 256, sched = one zeroed int
 int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* Dd,
-                    int64_t bh, int64_t N, int B, int width, const int32_t* counts, const int32_t* offsets,
+                    int64_t bh, int kv_group, int64_t N, int B, int width, const int32_t* counts, const int32_t* offsets,
                     const int32_t* flat, float scale, int* sched, float* dq_acc, float* dq_part,
                     int64_t part_stride, void* dk, void* dv, cudaStream_t s) {
     using namespace bwdp;
     static_assert(kSmem <= 232448, "backward smem budget");
     CUtensorMap tm_k, tm_v;
-    if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh * N), D, KT) || !make_tmap_bf16(&tm_v, v, (uint64_t)(bh * N), D, KT))
+    if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh / kv_group * N), D, KT) ||
+        !make_tmap_bf16(&tm_v, v, (uint64_t)(bh / kv_group * N), D, KT))
         return MOBA_ERR_CUDA;
     const int64_t n_items = bh * ceil_div(N, B) * ceil_div(B, KT);
     if (n_items >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
@@ -554,7 +555,7 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
     if (trace_path != nullptr && trace == nullptr) cudaMalloc(&trace, 256 * 16 * sizeof(long long));
     if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
     kern<<<grid, kThreads, kSmem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, bh,
-                                       N, B, width, counts, offsets, flat, scale, (int)n_items, sched, dq_acc, dq_part,
+                                       kv_group, N, B, width, counts, offsets, flat, scale, (int)n_items, sched, dq_acc, dq_part,
                                        part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                                        trace_path != nullptr ? trace : nullptr);
     int st = check_launch("moba_bwd_pipe_kernel");

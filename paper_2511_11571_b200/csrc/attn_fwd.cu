@@ -223,7 +223,7 @@ moba_fwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                    const __nv_bfloat16* __restrict__ V, int64_t N, int B, int BP, int width,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                    const int32_t* __restrict__ flat, const FwdItem* __restrict__ items,
-                   const int32_t* __restrict__ n_items_ptr, float scale_log2, uint32_t tmem_cols,
+                   const int32_t* __restrict__ n_items_ptr, float scale_log2, uint32_t tmem_cols, int kv_group,
                    __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse) {
     using namespace sm100;
     constexpr int SL = D / 64;  // 64-wide slabs of the head dim
@@ -285,8 +285,8 @@ moba_fwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
         }
         if (item.hj != cur_hj) {
             cur_hj = item.hj;
-            const __nv_bfloat16* Kh = K + (h * N + k0) * D;
-            const __nv_bfloat16* Vh = V + (h * N + k0) * D;
+            const __nv_bfloat16* Kh = K + ((h / kv_group) * N + k0) * D;   // GQA: K/V head of query head h
+            const __nv_bfloat16* Vh = V + ((h / kv_group) * N + k0) * D;
             for (int e = tid; e < BP * (D / 8); e += 128) {
                 const int r = e / (D / 8), c = e % (D / 8);
                 const bool ok = r < klen;
@@ -862,7 +862,7 @@ static FwdWs fwd_ws_layout(int64_t bh, int64_t N, int D, int B, int width) {
 }
 
 template <int D>
-int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
+int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int kv_group, int64_t N, int B, int width,
                   const int32_t* flat, const void* items, const int32_t* item_lo, const int32_t* item_hi,
                   float scale_log2, void* part_o, float* part_lse, cudaStream_t s);
 void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int32_t* item_off, int64_t total,
@@ -870,9 +870,10 @@ void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int3
 size_t fwd_ts_item_bytes();
 
 template <int D>
-static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
-                      const int32_t* counts, const int32_t* offsets, const int32_t* flat, const int32_t* row_pos,
-                      float scale, void* out, float* lse, uint8_t* ws, const FwdWs& L, cudaStream_t s) {
+static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, int kv_group, int64_t N, int B,
+                      int width, const int32_t* counts, const int32_t* offsets, const int32_t* flat,
+                      const int32_t* row_pos, float scale, void* out, float* lse, uint8_t* ws, const FwdWs& L,
+                      cudaStream_t s) {
     const int64_t n = ceil_div(N, B);
     const int64_t total = bh * n;
     int32_t* item_off = (int32_t*)(ws + L.item_off);
@@ -881,6 +882,9 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     const char* impl = std::getenv("MOBA_FWD_IMPL");
     const bool use_mma = impl != nullptr && impl[0] == 'm';
     const bool use_ts = ceil_div(B, 16) * 16 <= 128 && (impl == nullptr || impl[0] == 't');
+    // GQA (kv_group > 1) is wired into the default kernels (ping-pong ts for
+    // B <= 128, simple tcgen05 above); the legacy variants are MHA only
+    if (kv_group > 1 && (use_mma || (!use_ts && ceil_div(B, 16) * 16 <= 128))) return MOBA_ERR_UNSUPPORTED;
     const int bm = use_mma ? kFwdBM : kTcM;
     fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, bm, item_off, n_items);
     if (!use_ts) fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, bm, items);
@@ -903,7 +907,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
             const int64_t h1 = std::min(bh, h0 + hc);
             const int32_t* lo = item_off + h0 * n;
             const int32_t* hi = h1 < bh ? item_off + h1 * n : n_items;
-            st = launch_fwd_ts<D>(q, k, v, bh, N, B, width, flat, items, lo, hi, scale * kLog2e, ws + L.part_o,
+            st = launch_fwd_ts<D>(q, k, v, bh, kv_group, N, B, width, flat, items, lo, hi, scale * kLog2e, ws + L.part_o,
                                   (float*)(ws + L.part_lse), s);
             if (st) return st;
             StageTimer tm(T_COMBINE, s);
@@ -964,7 +968,7 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
         const int grid = (int)std::min<int64_t>(max_items, (int64_t)kNumSMs * occ);
         StageTimer tm(T_FWD, s);
         kern<<<grid, 128, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, N, B,
-                                     BP, width, counts, offsets, flat, items, n_items, scale * kLog2e, cols,
+                                     BP, width, counts, offsets, flat, items, n_items, scale * kLog2e, cols, kv_group,
                                      (__nv_bfloat16*)(ws + L.part_o), (float*)(ws + L.part_lse));
     }
     st = check_launch("moba_fwd_kernel");
@@ -984,11 +988,12 @@ extern "C" size_t moba_fwd_workspace_size(int64_t bh, int64_t n_tokens, int head
     return fwd_ws_layout(bh, n_tokens, head_dim, block_size, width).total;
 }
 
-extern "C" int moba_fwd(const void* q, const void* k, const void* v, int64_t bh, int64_t n_tokens, int head_dim,
-                        int block_size, int width, const int32_t* counts, const int32_t* offsets,
-                        const int32_t* flat, const int32_t* row_pos, float softmax_scale, void* out, float* lse,
-                        void* workspace, size_t workspace_bytes, void* stream) {
+extern "C" int moba_fwd_gqa(const void* q, const void* k, const void* v, int64_t bh, int kv_group, int64_t n_tokens,
+                            int head_dim, int block_size, int width, const int32_t* counts, const int32_t* offsets,
+                            const int32_t* flat, const int32_t* row_pos, float softmax_scale, void* out, float* lse,
+                            void* workspace, size_t workspace_bytes, void* stream) {
     if (bh < 1 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
+    if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
     if (width > 32 || block_size > 256) return MOBA_ERR_UNSUPPORTED;
     if (n_tokens * width >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
     FwdWs L = fwd_ws_layout(bh, n_tokens, head_dim, block_size, width);
@@ -996,10 +1001,18 @@ extern "C" int moba_fwd(const void* q, const void* k, const void* v, int64_t bh,
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = (uint8_t*)workspace;
     if (head_dim == 64)
-        return launch_fwd<64>(q, k, v, bh, n_tokens, block_size, width, counts, offsets, flat, row_pos,
+        return launch_fwd<64>(q, k, v, bh, kv_group, n_tokens, block_size, width, counts, offsets, flat, row_pos,
                               softmax_scale, out, lse, ws, L, s);
     if (head_dim == 128)
-        return launch_fwd<128>(q, k, v, bh, n_tokens, block_size, width, counts, offsets, flat, row_pos,
+        return launch_fwd<128>(q, k, v, bh, kv_group, n_tokens, block_size, width, counts, offsets, flat, row_pos,
                                softmax_scale, out, lse, ws, L, s);
     return MOBA_ERR_UNSUPPORTED;
+}
+
+extern "C" int moba_fwd(const void* q, const void* k, const void* v, int64_t bh, int64_t n_tokens, int head_dim,
+                        int block_size, int width, const int32_t* counts, const int32_t* offsets,
+                        const int32_t* flat, const int32_t* row_pos, float softmax_scale, void* out, float* lse,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+    return moba_fwd_gqa(q, k, v, bh, 1, n_tokens, head_dim, block_size, width, counts, offsets, flat, row_pos,
+                        softmax_scale, out, lse, workspace, workspace_bytes, stream);
 }

@@ -94,7 +94,7 @@ MOBA_DEV Item load_item(const Item* p) {
 template <int D, int NCH>
 __global__ void __launch_bounds__(kThreads, 1)
 moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width,
+                   const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width, int kv_group,
                    const int32_t* __restrict__ flat, const Item* __restrict__ items,
                    const int32_t* __restrict__ item_lo, const int32_t* __restrict__ item_hi, float scale_log2,
                    __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse,
@@ -189,8 +189,10 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                         const uint32_t kb = sbase + oKV + ks * 2 * kv_bytes;
 #pragma unroll
                         for (int sl = 0; sl < SL; ++sl) {
-                            tma_load_3d(kb + sl * BP * 128, &tm_k, sl * 64, j * B, (int)h, &bars->kv_full[ks]);
-                            tma_load_3d(kb + kv_bytes + sl * BP * 128, &tm_v, sl * 64, j * B, (int)h,
+                            // GQA: query head h reads K/V head h / kv_group
+                            const int hk = (int)(h / kv_group);
+                            tma_load_3d(kb + sl * BP * 128, &tm_k, sl * 64, j * B, hk, &bars->kv_full[ks]);
+                            tma_load_3d(kb + kv_bytes + sl * BP * 128, &tm_v, sl * 64, j * B, hk,
                                         &bars->kv_full[ks]);
                         }
                     }
@@ -508,15 +510,15 @@ void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int3
 // d in {64, 128}, ceil16(B) <= 128; runs the items [*item_lo, *item_hi)
 // (device values) — a contiguous range of heads.
 template <int D>
-int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64_t N, int B, int width,
+int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int kv_group, int64_t N, int B, int width,
                   const int32_t* flat, const void* items, const int32_t* item_lo, const int32_t* item_hi,
                   float scale_log2, void* part_o, float* part_lse, cudaStream_t s) {
     using namespace fwdts;
     const int BP = (int)ceil_div(B, 16) * 16;
     if (BP > 128) return MOBA_ERR_UNSUPPORTED;
     CUtensorMap tm_k, tm_v;
-    if (!make_tmap_bf16_3d(&tm_k, k, (uint64_t)bh, (uint64_t)N, D, BP) ||
-        !make_tmap_bf16_3d(&tm_v, v, (uint64_t)bh, (uint64_t)N, D, BP))
+    if (!make_tmap_bf16_3d(&tm_k, k, (uint64_t)(bh / kv_group), (uint64_t)N, D, BP) ||
+        !make_tmap_bf16_3d(&tm_v, v, (uint64_t)(bh / kv_group), (uint64_t)N, D, BP))
         return MOBA_ERR_CUDA;
     CUtensorMap tm_po;
     if (!make_tmap_bf16(&tm_po, part_o, (uint64_t)(bh * N * width), D, 32)) return MOBA_ERR_CUDA;
@@ -536,7 +538,7 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
     if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
     {
         StageTimer tm(T_FWD, s);
-        kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, flat,
+        kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, kv_group, flat,
                                           (const Item*)items, item_lo, item_hi, scale_log2, (__nv_bfloat16*)part_o,
                                           part_lse, tm_po, trace_path != nullptr ? trace : nullptr);
     }
@@ -553,9 +555,11 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int64
     return st;
 }
 
-template int launch_fwd_ts<64>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,
-                               const void*, const int32_t*, const int32_t*, float, void*, float*, cudaStream_t);
-template int launch_fwd_ts<128>(const void*, const void*, const void*, int64_t, int64_t, int, int, const int32_t*,
-                                const void*, const int32_t*, const int32_t*, float, void*, float*, cudaStream_t);
+template int launch_fwd_ts<64>(const void*, const void*, const void*, int64_t, int, int64_t, int, int,
+                               const int32_t*, const void*, const int32_t*, const int32_t*, float, void*, float*,
+                               cudaStream_t);
+template int launch_fwd_ts<128>(const void*, const void*, const void*, int64_t, int, int64_t, int, int,
+                                const int32_t*, const void*, const int32_t*, const int32_t*, float, void*, float*,
+                                cudaStream_t);
 
 }  // namespace moba

@@ -93,7 +93,7 @@ MOBA_DEV void select_chunk32(const float (&sv)[32], int j0, int lim, float (&ts)
 template <int D, int KMAX>
 __global__ void __launch_bounds__(kRouteThreads)
 route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, int64_t N,
-                       int B, int top_k, int32_t* __restrict__ topk) {
+                       int B, int top_k, int kv_group, int32_t* __restrict__ topk) {
     extern __shared__ __align__(16) float route_smem[];
     float (*q_s)[kRouteQ] = reinterpret_cast<float (*)[kRouteQ]>(route_smem);
     float (*c_s)[kRouteC] = reinterpret_cast<float (*)[kRouteC]>(route_smem + D * kRouteQ);
@@ -107,7 +107,7 @@ route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restr
     const int n_blocks = (int)((N + B - 1) / B);
     const int width = top_k + 1;
     const __nv_bfloat16* Qh = Q + h * N * D;
-    const float* Ch = cent + (int64_t)h * n_blocks * D;
+    const float* Ch = cent + (int64_t)(h / kv_group) * n_blocks * D;   // GQA: the query head's K/V head
 
     // stage the query tile transposed (fp32, exact)
     for (int e = tid; e < kRouteQ * (D / 8); e += kRouteThreads) {
@@ -240,7 +240,7 @@ constexpr int kRtN = 64;    // centroids per chunk (MMA N)
 template <int D, int KMAX>
 __global__ void __launch_bounds__(128)
 route_topk_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
-                     int B, int top_k, int64_t split_rows, int32_t* __restrict__ topk) {
+                     int B, int top_k, int64_t split_rows, int kv_group, int32_t* __restrict__ topk) {
     using namespace sm100;
     constexpr int SL = D / 64;
     constexpr uint32_t q_bytes = kRtM * D * 2;
@@ -287,7 +287,7 @@ route_topk_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 #pragma unroll
             for (int sl = 0; sl < SL; ++sl)
                 tma_load_2d(cb + term * c_bytes + sl * kRtN * 128, &tm_c, sl * 64,
-                            (int)(term * split_rows + h * n_blocks + (int64_t)c * kRtN), &bars[buf]);
+                            (int)(term * split_rows + (h / kv_group) * n_blocks + (int64_t)c * kRtN), &bars[buf]);
     };
     auto issue_mma = [&](int c) {             // thread 0
         const int buf = c & 1;
@@ -410,7 +410,7 @@ MOBA_DEV void select_chunk16(const float* sv, int j0, int lim, float (&ts)[KMAX]
 template <int D, int KMAX>
 __global__ void __launch_bounds__(kRt2Threads)
 route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
-                      int B, int top_k, int64_t split_rows, int32_t* __restrict__ topk) {
+                      int B, int top_k, int64_t split_rows, int kv_group, int32_t* __restrict__ topk) {
     using namespace sm100;
     constexpr int SL = D / 64;
     constexpr uint32_t q_bytes = kRtM * D * 2;
@@ -458,7 +458,7 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 #pragma unroll
             for (int sl = 0; sl < SL; ++sl)
                 tma_load_2d(cb + term * c_bytes + sl * kRtN * 128, &tm_c, sl * 64,
-                            (int)(term * split_rows + h * n_blocks + (int64_t)c * kRtN), &bars[buf]);
+                            (int)(term * split_rows + (h / kv_group) * n_blocks + (int64_t)c * kRtN), &bars[buf]);
     };
     auto issue_mma = [&](int c) {             // thread 0
         const int buf = c & 1;
@@ -862,50 +862,51 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
 
 template <int D, int KMAX>
 static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k, int mode,
-                        int32_t* topk, void* split_ws, cudaStream_t s) {
+                        int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
     dim3 grid((unsigned)ceil_div(N, kRouteQ), (unsigned)bh);
     if (mode == MOBA_ROUTE_TC) {
         const int64_t n = ceil_div(N, B);
-        const int64_t total = bh * n * D;
+        const int64_t bh_kv = bh / kv_group;
+        const int64_t total = bh_kv * n * D;
         __nv_bfloat16* split = (__nv_bfloat16*)split_ws;
         centroid_split_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(cent, total, split);
         int st = check_launch("centroid_split_kernel");
         if (st) return st;
         CUtensorMap tm_q, tm_c;
         if (!make_tmap_bf16(&tm_q, q, (uint64_t)(bh * N), D, kRtM) ||
-            !make_tmap_bf16(&tm_c, split, (uint64_t)(3 * bh * n), D, kRtN))
+            !make_tmap_bf16(&tm_c, split, (uint64_t)(3 * bh_kv * n), D, kRtN))
             return MOBA_ERR_CUDA;
         const char* impl = std::getenv("MOBA_ROUTE_IMPL");
         if (impl != nullptr && impl[0] == '1') {
             const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 4 * 33 * 33 * 4;
             auto kern = route_topk_tc_kernel<D, KMAX>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh * n, topk);
+            kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, topk);
             return check_launch("route_topk_tc_kernel");
         }
         static_assert(2 * 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the C buffers");
         const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
         auto kern = route_topk_tc2_kernel<D, KMAX>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh * n, topk);
+        kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, topk);
         return check_launch("route_topk_tc2_kernel");
     }
     const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
     cudaFuncSetAttribute(route_topk_fp32_kernel<D, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     route_topk_fp32_kernel<D, KMAX><<<grid, kRouteThreads, smem, s>>>((const __nv_bfloat16*)q, cent, N, B,
-                                                                       top_k, topk);
+                                                                       top_k, kv_group, topk);
     return check_launch("route_topk_fp32_kernel");
 }
 
 template <int D>
 static int dispatch_route_k(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k, int mode,
-                            int32_t* topk, void* split_ws, cudaStream_t s) {
-    if (top_k <= 1) return launch_route<D, 1>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
-    if (top_k <= 2) return launch_route<D, 2>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
-    if (top_k <= 4) return launch_route<D, 4>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
-    if (top_k <= 8) return launch_route<D, 8>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
-    if (top_k <= 16) return launch_route<D, 16>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
-    if (top_k <= 32) return launch_route<D, 32>(q, cent, bh, N, B, top_k, mode, topk, split_ws, s);
+                            int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
+    if (top_k <= 1) return launch_route<D, 1>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
+    if (top_k <= 2) return launch_route<D, 2>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
+    if (top_k <= 4) return launch_route<D, 4>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
+    if (top_k <= 8) return launch_route<D, 8>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
+    if (top_k <= 16) return launch_route<D, 16>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
+    if (top_k <= 32) return launch_route<D, 32>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
     return MOBA_ERR_UNSUPPORTED;
 }
 
@@ -925,11 +926,12 @@ extern "C" size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int bl
     return varlen_ws_bytes(bh, n_tokens, block_size) + 3 * (size_t)bh * ceil_div(n_tokens, block_size) * 128 * 2;
 }
 
-extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int64_t n_tokens, int head_dim,
-                          int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
-                          int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
-                          size_t workspace_bytes, void* stream) {
+extern "C" int moba_route_gqa(const void* q, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
+                              int head_dim, int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
+                              int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
+                              size_t workspace_bytes, void* stream) {
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1) return MOBA_ERR_SHAPE;
+    if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
     if (top_k < 1) return MOBA_ERR_CONFIG;
     if (top_k > 31) return MOBA_ERR_UNSUPPORTED;
     if (mode != MOBA_ROUTE_FP32 && mode != MOBA_ROUTE_TC) return MOBA_ERR_CONFIG;
@@ -939,13 +941,23 @@ extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int
     StageTimer tm(T_ROUTE, s);
     if (workspace_bytes < moba_route_workspace_size(bh, n_tokens, block_size, top_k)) return MOBA_ERR_WORKSPACE;
     void* split_ws = (char*)workspace + varlen_ws_bytes(bh, n_tokens, block_size);
-    if (head_dim == 64) st = dispatch_route_k<64>(q, centroids, bh, n_tokens, block_size, top_k, mode, topk, split_ws, s);
-    else if (head_dim == 128) st = dispatch_route_k<128>(q, centroids, bh, n_tokens, block_size, top_k, mode, topk, split_ws, s);
+    if (head_dim == 64)
+        st = dispatch_route_k<64>(q, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk, split_ws, s);
+    else if (head_dim == 128)
+        st = dispatch_route_k<128>(q, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk, split_ws, s);
     else return MOBA_ERR_UNSUPPORTED;
     }
     if (st) return st;
     return run_varlen(topk, bh, n_tokens, top_k + 1, block_size, counts, offsets, flat, row_pos, workspace,
                       workspace_bytes, s, false);
+}
+
+extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int64_t n_tokens, int head_dim,
+                          int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
+                          int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    return moba_route_gqa(q, centroids, bh, 1, n_tokens, head_dim, block_size, top_k, mode, topk, counts, offsets,
+                          flat, row_pos, workspace, workspace_bytes, stream);
 }
 
 extern "C" int moba_varlen(const int32_t* topk, int64_t bh, int64_t n_tokens, int width, int block_size,

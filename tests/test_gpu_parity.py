@@ -398,3 +398,55 @@ def test_graphed_step_matches_eager(conv):
         ref.backward(do)
         for got, exp, nm in ((out, ref, "O"), (dq, qg.grad, "dQ"), (dk, kg.grad, "dK"), (dv, vg.grad, "dV")):
             assert torch.equal(got, exp), (trial, nm)
+
+
+@pytest.mark.parametrize("hq,hkv,d,B", [(8, 2, 64, 128), (4, 1, 64, 64), (4, 2, 128, 128)])
+def test_gqa_matches_expanded_heads(hq, hkv, d, B):
+    """GQA/MQA: K/V heads shared by hq/hkv query heads give
+    the same O/LSE/dQ as running MHA on repeated K/V heads, and dK/dV equal
+    the per-group sums of the repeated heads' gradients."""
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    N, k = 1280, 4
+    G = hq // hkv
+    q, do = (torch.randn(2, hq, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    kk, v = (torch.randn(2, hkv, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
+    out, lse = mb.moba_attn(qg, kg, vg, B, k, mode="fp32", deterministic=True, return_lse=True)
+    out.backward(do)
+    qe = q.clone().requires_grad_(True)
+    ke = kk.repeat_interleave(G, dim=1).requires_grad_(True)
+    ve = v.repeat_interleave(G, dim=1).requires_grad_(True)
+    oe, lse_e = mb.moba_attn(qe, ke, ve, B, k, mode="fp32", deterministic=True, return_lse=True)
+    oe.backward(do)
+    assert torch.equal(out, oe) and torch.equal(lse, lse_e)
+    assert torch.equal(qg.grad, qe.grad)
+    for got, exp, nm in ((kg.grad, ke.grad, "dK"), (vg.grad, ve.grad, "dV")):
+        ref = exp.float().view(2, hkv, G, N, d).sum(2).bfloat16().float()   # one bf16 rounding of the sum
+        assert got.shape == kk.shape
+        assert_close(got.float().cpu().numpy(), ref.cpu().numpy(), nm, max_abs=1e-2, rel=1e-3)
+
+
+def test_gqa_vs_oracle():
+    """GQA against the CPU oracle: each query head attends with its K/V
+    head; dK/dV of a K/V head = sum of the oracle's per-query-head dK/dV."""
+    gen = torch.Generator(device="cuda").manual_seed(22)
+    hq, hkv, N, d, B, k = 4, 2, 700, 64, 64, 3
+    q, do = (torch.randn(hq, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    kk, v = (torch.randn(hkv, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
+    out = mb.moba_attn(qg, kg, vg, B, k, mode="fp32", deterministic=True)
+    out.backward(do)
+    Qn, Kn, Vn, dOn = (t.double().cpu().numpy() for t in (q, kk, v, do))
+    dK = np.zeros_like(Kn)
+    dV = np.zeros_like(Vn)
+    for h in range(hq):
+        hk = h // (hq // hkv)
+        plan = orc.build_plan(Qn[h], Kn[hk], B, k)
+        O, L = orc.forward(Qn[h], Kn[hk], Vn[hk], plan, B)
+        dq, dk, dv = orc.backward(Qn[h], Kn[hk], Vn[hk], O, dOn[h], L, plan, B)
+        assert_close(out[h].detach().double().cpu().numpy(), O, f"O[{h}]")
+        assert_close(qg.grad[h].double().cpu().numpy(), dq, f"dQ[{h}]")
+        dK[hk] += dk
+        dV[hk] += dv
+    assert_close(kg.grad.double().cpu().numpy(), dK, "dK")
+    assert_close(vg.grad.double().cpu().numpy(), dV, "dV")
