@@ -450,3 +450,26 @@ def test_gqa_vs_oracle():
         dV[hk] += dv
     assert_close(kg.grad.double().cpu().numpy(), dK, "dK")
     assert_close(vg.grad.double().cpu().numpy(), dV, "dV")
+
+
+def test_hybrid_lm_train_step():
+    """C5 layer stack at toy size: SWA+RoPE / MoBA(+kconv3)
+    alternating layers train end to end through the MoBA kernels (loss falls
+    on a repeated batch; every MoBA-layer parameter gets a finite gradient)."""
+    pytest.importorskip("flash_attn")
+    from paper_2511_11571_b200.lm import MobaLM, MobaLMConfig, train_step
+    torch.manual_seed(0)
+    cfg = MobaLMConfig(vocab=512, hidden=256, heads=4, head_dim=64, intermediate=512, layers=4, block_size=128,
+                       top_k=4, conv_width=3)
+    model = MobaLM(cfg).cuda().to(torch.bfloat16)
+    opt = torch.optim.AdamW(model.parameters(), lr=3e-3)
+    tokens = torch.randint(0, cfg.vocab, (2, 1024), device="cuda")
+    losses = [float(train_step(model, opt, tokens)) for _ in range(12)]
+    assert all(np.isfinite(losses)), losses
+    assert min(losses[-3:]) < losses[0] - 0.2, losses
+    model.zero_grad()
+    model.loss(tokens).backward()
+    blk = model.blocks[1]            # layer 2: MoBA with key conv
+    assert blk.attn.moba and blk.attn.conv is not None
+    for name, p in blk.named_parameters():
+        assert p.grad is not None and bool(torch.isfinite(p.grad).all()) and float(p.grad.abs().sum()) > 0, name
