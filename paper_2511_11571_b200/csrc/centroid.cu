@@ -94,6 +94,55 @@ centroid_conv_kernel(const __nv_bfloat16* __restrict__ K, const float* __restric
     }
 }
 
+// Plain centroids (no conv): one warp per (head, block). L = D/8 lanes cover
+// a 16-B-per-lane row, 32/L rows per warp step, 8 steps of loads in flight
+// per lane before any is summed; lane groups are folded with shuffles. The
+// per-column summation order is fixed (deterministic).
+template <int D>
+__global__ void __launch_bounds__(256)
+centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int64_t total_blocks,
+                     float* __restrict__ cent) {
+    constexpr int L = D / 8, G = 32 / L, U = 8;
+    const int64_t wb = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (wb >= total_blocks) return;
+    const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int64_t h = wb / n_blocks;
+    const int j = (int)(wb - h * n_blocks);
+    const int64_t t0 = (int64_t)j * B;
+    const int len = (int)min64(B, N - t0);
+    const uint4* base = reinterpret_cast<const uint4*>(K + (h * N + t0) * D) + sub;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r0 = grp; r0 < len; r0 += U * G) {
+        uint4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = r0 + u * G;
+            raw[u] = (r < len) ? __ldg(base + (int64_t)r * L) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float2 f = unpack_bf16(w4[c]);
+                acc[2 * c] += f.x;
+                acc[2 * c + 1] += f.y;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if (grp == 0) {
+        const float inv = 1.f / (float)len;
+        float4* dst = reinterpret_cast<float4*>(cent + wb * D + sub * 8);
+        dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+        dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    }
+}
+
 // ---------------------------------------------------------------- conv backward
 // key_conv_backward (src/keyconv.py:81-104). One CTA per (head, 64-row
 // chunk): g over the chunk plus a (width-1)-row lookahead in smem, then
@@ -187,6 +236,17 @@ extern "C" int moba_centroids(const void* k, const float* conv_w, int conv_width
     const int RG = kCentThreads / (head_dim / 8);
     size_t smem = (size_t)RG * head_dim * sizeof(float);
     StageTimer tm(T_CENTROID, (cudaStream_t)stream);
+    if (conv_width == 0 && (head_dim == 64 || head_dim == 128)) {
+        const int64_t total = bh * n_blocks;
+        const unsigned g = (unsigned)ceil_div(total, 8);
+        if (head_dim == 64)
+            centroid_warp_kernel<64><<<g, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
+                                                                         block_size, total, centroids);
+        else
+            centroid_warp_kernel<128><<<g, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
+                                                                          block_size, total, centroids);
+        return check_launch("centroid_warp_kernel");
+    }
     centroid_conv_kernel<<<grid, kCentThreads, smem, (cudaStream_t)stream>>>(
         (const __nv_bfloat16*)k, conv_w, conv_width, n_tokens, head_dim, block_size,
         (__nv_bfloat16*)k_conv_out, centroids);

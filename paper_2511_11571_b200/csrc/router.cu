@@ -702,19 +702,27 @@ varlen_scatter_kernel(const int32_t* __restrict__ topk, int64_t N, int width, in
     int32_t* rp = row_pos + (h * N + i0) * width;
     int32_t* fl = flat + h * N * width;
     if (tid < 32) {
-        // width <= 32: lane = slot; one query at a time keeps every block's
-        // slice in ascending query order (a row never repeats a block)
-        const int s = tid;
-        for (int q = 0; q < nq; ++q) {
-            const int32_t b = (s < width) ? rows_s[q * width + s] : -1;
+        // Entries in (query, slot) order, 32 per step: lanes holding the same
+        // block (__match_any_sync) rank themselves by lane = entry order =
+        // query order (a row never repeats a block), so every block's slice
+        // comes out strictly ascending, as the reference's cursor walk
+        // (src/router.py:143-148).
+        const int lane = tid;
+        const int ne = nq * width;
+        const unsigned lt = (1u << lane) - 1u;
+        for (int e0 = 0; e0 < ne; e0 += 32) {
+            const int e = e0 + lane;
+            const int32_t b = (e < ne) ? rows_s[e] : -1;
+            const unsigned grp = __match_any_sync(0xffffffffu, b);
+            int32_t p = -1;
             if (b >= 0) {
-                const int32_t p = cursor[b];
-                cursor[b] = p + 1;
-                fl[p] = (int32_t)(i0 + q);
-                rows_s[q * width + s] = p;
-            } else if (s < width) {
-                rows_s[q * width + s] = -1;
+                const int32_t base = cursor[b];
+                p = base + __popc(grp & lt);
+                fl[p] = (int32_t)(i0 + e / width);
             }
+            __syncwarp();
+            if (b >= 0 && (grp & lt) == 0) cursor[b] += __popc(grp);   // group leader advances the cursor
+            if (e < ne) rows_s[e] = p;
             __syncwarp();
         }
     }
