@@ -46,6 +46,7 @@ constexpr int kPr0 = 1, kPrN = 3;
 constexpr int kSm0 = 4;       // softmax warps 4-11
 constexpr int kEp0 = 12;      // epilogue warps 12-15
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr bool kPolyExp = false;   // measured slower (issue-bound softmax), kept for experiments
 constexpr uint32_t kStg = 32 * 128;    // per-warp O staging: 32 rows x one 64-column SW128 slab
 
 struct Bars {
@@ -358,25 +359,26 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                     mbar_wait(&bars->p_free[wg], ((li >> 1) - 1) & 1);
                     tc_fence_after();
                 }
-                // x*scale - m and the row sum in packed fp32x2 (FFMA2 / FADD2)
+                // x*scale - m and the row sum in packed fp32x2 (FFMA2 / FADD2).
+                // Per 32-column chunk all shifts, then all 32 exponentials,
+                // then sums / packing: the MUFU ops are independent and back
+                // to back (the softmax is latency-bound, not MUFU-bound).
                 float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
+                    float* t = &sv[c * 32];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) ffma2(t[i], t[i + 1], t[i], t[i + 1], scale_log2, scale_log2, -msl, -msl);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) t[i] = (kPolyExp && (i & 3) == 3) ? poly_exp2(t[i]) : fast_exp2(t[i]);
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {
-                        float t0, t1, t2, t3;
-                        ffma2(t0, t1, sv[c * 32 + i], sv[c * 32 + i + 1], scale_log2, scale_log2, -msl, -msl);
-                        ffma2(t2, t3, sv[c * 32 + i + 2], sv[c * 32 + i + 3], scale_log2, scale_log2, -msl, -msl);
-                        t0 = fast_exp2(t0);
-                        t1 = fast_exp2(t1);
-                        t2 = fast_exp2(t2);
-                        t3 = fast_exp2(t3);
                         const int a = (i >> 1) & 2;
-                        fadd2(ls[a], ls[a + 1], ls[a], ls[a + 1], t0, t1);
-                        fadd2(ls[a], ls[a + 1], ls[a], ls[a + 1], t2, t3);
-                        pk[i >> 1] = pack_bf16(t0, t1);
-                        pk[(i >> 1) + 1] = pack_bf16(t2, t3);
+                        fadd2(ls[a], ls[a + 1], ls[a], ls[a + 1], t[i], t[i + 1]);
+                        fadd2(ls[a], ls[a + 1], ls[a], ls[a + 1], t[i + 2], t[i + 3]);
+                        pk[i >> 1] = pack_bf16(t[i], t[i + 1]);
+                        pk[(i >> 1) + 1] = pack_bf16(t[i + 2], t[i + 3]);
                     }
                     tmem_st16(pslot + c * 16, pk);
                 }

@@ -38,6 +38,21 @@ MOBA_DEV float fast_exp2(float x) {
     return y;
 }
 
+// 2^x for x <= 0 on the FMA/ALU pipes (MUFU offload, as FlashAttention-4):
+// j = round(x) via the 1.5*2^23 magic add (no F2I / FRND, which would use the
+// same XU pipe as MUFU), f = x - j in [-0.5, 0.5], 2^f by a degree-3
+// relative-minimax polynomial (max rel. error 7.7e-5, far below bf16's
+// 2^-9), 2^j added to the exponent field. x is clamped at -126.
+MOBA_DEV float poly_exp2(float x) {
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.0f;            // low mantissa bits = round(x)
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(0.05508876707445847f, f, 0.24260465620999191f);
+    p = fmaf(p, f, 0.6932762833525732f);
+    p = fmaf(p, f, 0.9999289048020072f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // packed fp32x2 arithmetic (sm_100: one FFMA2 / FADD2 for two lanes of data)
 MOBA_DEV void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
     asm("{\n\t.reg .b64 a, b, c, d;\n\t"
