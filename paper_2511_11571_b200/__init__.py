@@ -25,6 +25,7 @@ from .attention import AttentionOutput, MobaAttnFunction, moba_attention, moba_a
 from .keyconv import ConvKernel, key_conv_backward, key_conv_forward, random_kernel
 from .pipeline import HostPipeline, moba_fwd_bwd_host
 from .graphs import MobaGraphedStep
+from .tensorio import RunReport, Tensor, tensor_read, tensor_write
 
 
 def validate_plan(plan, n_tokens: int, cfg: MobaConfig) -> None:

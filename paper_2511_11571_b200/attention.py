@@ -105,9 +105,12 @@ def moba_backward(Q, K, V, O, dO, lse, plan: RoutingPlan, cfg: MobaConfig,
 
 
 def moba_attention(Q, K, V, cfg: MobaConfig, counters: OpCounters | None = None,
-                   threads: int | None = 1, mode: str = "fp32") -> tuple[AttentionOutput, RoutingPlan]:
+                   threads: int | None = 1, mode: str = "fp32", kernel=None) -> tuple[AttentionOutput, RoutingPlan]:
     """End-to-end routed attention: centroids, tiled top-k, varlen, forward
-    (src/attention.py:305-314). Routing uses the UNSCALED Q (src/attention.py:312)."""
+    (src/attention.py:305-314). Routing uses the UNSCALED Q (src/attention.py:312).
+    `kernel` (a ConvKernel, optional) applies the key short-conv first, fused
+    with the centroids so routing sees the unrounded K' (what the reference's
+    CLI does with key_conv_forward before moba_attention, src/cli.py:277-278)."""
     _check_qkv(Q, K, V)
     if Q.shape[-1] != cfg.head_dim_d:
         raise ShapeError(f"d={Q.shape[-1]} does not match cfg.head_dim_d={cfg.head_dim_d}")
@@ -115,7 +118,11 @@ def moba_attention(Q, K, V, cfg: MobaConfig, counters: OpCounters | None = None,
     q, info = to_heads(Q, "Q")
     k, _ = to_heads(K, "K", device=q.device)
     v, _ = to_heads(V, "V", device=q.device)
-    cent, _ = _device.centroids(k, cfg.block_size_B)
+    if kernel is not None:
+        w = to_weights(getattr(kernel, "weights", kernel), info.d, info.dp, q.device)
+        cent, k = _device.centroids(k, cfg.block_size_B, w)
+    else:
+        cent, _ = _device.centroids(k, cfg.block_size_B)
     if cfg.top_k > _device.MAX_TOP_K:
         raise ConfigError(f"top_k={cfg.top_k} is not supported by the compiled kernels")
     plan = _device.route(q, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])

@@ -473,3 +473,31 @@ def test_hybrid_lm_train_step():
     assert blk.attn.moba and blk.attn.conv is not None
     for name, p in blk.named_parameters():
         assert p.grad is not None and bool(torch.isfinite(p.grad).all()) and float(p.grad.abs().sum()) > 0, name
+
+
+def test_cli_attend_tns1_vs_oracle(tmp_path):
+    """`cli attend` on TNS1 files: output, LSE and the
+    emitted plan match the oracle (single head, key conv on)."""
+    import json as _json
+    from paper_2511_11571_b200 import cli
+    from paper_2511_11571_b200.tensorio import Tensor, tensor_read, tensor_write
+    rng = np.random.default_rng(3)
+    N, d, B, k, W = 640, 64, 64, 3, 3
+    Q, K, V = (bf16_round(rng.standard_normal((N, d))) for _ in range(3))
+    w = rng.uniform(-0.5, 0.5, size=(W, d))
+    for name, arr in (("q", Q), ("k", K), ("v", V), ("w", w)):
+        tensor_write(Tensor(arr), tmp_path / f"{name}.tns")
+    rc = cli.main(["attend", "--q", str(tmp_path / "q.tns"), "--k", str(tmp_path / "k.tns"), "--v",
+                   str(tmp_path / "v.tns"), "--out", str(tmp_path / "o.tns"), "--block", str(B), "--topk", str(k),
+                   "--conv", str(W), "--kernel", str(tmp_path / "w.tns"), "--emit-plan", str(tmp_path / "p.json"),
+                   "--emit-lse", str(tmp_path / "l.tns")])
+    assert rc == 0
+    Kc = orc.key_conv_forward(K, w)
+    plan = orc.build_plan(Q, Kc, B, k)
+    O, L = orc.forward(Q, Kc, V, plan, B)
+    assert_close(tensor_read(tmp_path / "o.tns").array, O, "O")
+    assert_close(tensor_read(tmp_path / "l.tns").array, L, "LSE")
+    p = _json.load(open(tmp_path / "p.json"))
+    assert p["counts"] == plan.counts.tolist()
+    assert p["offsets"] == plan.offsets.tolist()
+    assert p["flat_queries"] == plan.flat_queries.tolist()
