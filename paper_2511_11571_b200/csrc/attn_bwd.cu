@@ -667,31 +667,42 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 
 // D = rowsum(dO * O) and dq_acc = 0; one warp per row.
 template <int D>
+// D = rowsum(dO * O) (src/attention.py:266) and dQ accumulator zeroing:
+// D/8 lanes per row, 16-B loads and stores, 32/(D/8) rows per warp.
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ O, const __nv_bfloat16* __restrict__ dO,
                                       int64_t rows, float* __restrict__ Dd, float* __restrict__ dq_acc) {
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    constexpr int PER = D / 32;
+    constexpr int L = D / 8, G = 32 / L;
+    const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
+    const int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G + grp;
+    const bool ok = row < rows;
+    const int64_t r = ok ? row : 0;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(O + r * D) + sub);
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(dO + r * D) + sub);
+    const uint32_t ua[4] = {a.x, a.y, a.z, a.w}, ub[4] = {b.x, b.y, b.z, b.w};
     float s = 0.f;
 #pragma unroll
-    for (int c = 0; c < PER; c += 2) {
-        float2 a = unpack_bf16(*reinterpret_cast<const uint32_t*>(O + row * D + lane * PER + c));
-        float2 b = unpack_bf16(*reinterpret_cast<const uint32_t*>(dO + row * D + lane * PER + c));
-        s = fmaf(a.x, b.x, fmaf(a.y, b.y, s));
+    for (int c = 0; c < 4; ++c) {
+        const float2 x = unpack_bf16(ua[c]), y = unpack_bf16(ub[c]);
+        s = fmaf(x.x, y.x, fmaf(x.y, y.y, s));
     }
-    s = warp_sum(s);
-    if (lane == 0) Dd[row] = s;
 #pragma unroll
-    for (int c = 0; c < PER; ++c) dq_acc[row * D + lane * PER + c] = 0.f;
+    for (int o = 1; o < L; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (ok) {
+        if (sub == 0) Dd[row] = s;
+        float4* z = reinterpret_cast<float4*>(dq_acc + row * D + sub * 8);
+        z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 }
 
 __global__ void bwd_finalize_kernel(const float* __restrict__ dq_acc, int64_t n, float scale,
                                     __nv_bfloat16* __restrict__ dQ) {
-    int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (e >= n) return;
-    float4 v = *reinterpret_cast<const float4*>(dq_acc + e);
-    *reinterpret_cast<uint2*>(dQ + e) = make_uint2(pack_bf16(v.x * scale, v.y * scale), pack_bf16(v.z * scale, v.w * scale));
+    const float4 v = __ldg(reinterpret_cast<const float4*>(dq_acc + e));
+    const float4 w = __ldg(reinterpret_cast<const float4*>(dq_acc + e) + 1);
+    *reinterpret_cast<uint4*>(dQ + e) = make_uint4(pack_bf16(v.x * scale, v.y * scale), pack_bf16(v.z * scale, v.w * scale),
+                                                   pack_bf16(w.x * scale, w.y * scale), pack_bf16(w.z * scale, w.w * scale));
 }
 
 // deterministic dQ: per query, sum its partials in (slot, slab) order.
@@ -801,7 +812,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     }
     {
     StageTimer tm(T_BWD_PRE, s);
-    bwd_preprocess_kernel<D><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>((const __nv_bfloat16*)out,
+    bwd_preprocess_kernel<D><<<(unsigned)ceil_div(rows, 8 * (256 / D)), 256, 0, s>>>((const __nv_bfloat16*)out,
                                                                         (const __nv_bfloat16*)dout, rows, Dd, dq_acc);
     }
     int st = check_launch("bwd_preprocess_kernel");
@@ -871,7 +882,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         return check_launch("bwd_dq_combine_kernel");
     }
     const int64_t ne = rows * D;
-    bwd_finalize_kernel<<<(unsigned)ceil_div(ne / 4, 256), 256, 0, s>>>(dq_acc, ne, scale, (__nv_bfloat16*)dq);
+    bwd_finalize_kernel<<<(unsigned)ceil_div(ne / 8, 256), 256, 0, s>>>(dq_acc, ne, scale, (__nv_bfloat16*)dq);
     return check_launch("bwd_finalize_kernel");
 }
 
