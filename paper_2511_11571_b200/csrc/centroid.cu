@@ -94,18 +94,19 @@ centroid_conv_kernel(const __nv_bfloat16* __restrict__ K, const float* __restric
     }
 }
 
-// Plain centroids (no conv): one warp per (head, block). L = D/8 lanes cover
-// a 16-B-per-lane row, 32/L rows per warp step, 8 steps of loads in flight
-// per lane before any is summed; lane groups are folded with shuffles. The
+// Plain centroids (no conv): one 4-warp CTA per (head, block). L = D/8
+// lanes cover a 16-B-per-lane row, each warp takes every 4th group of 32/L
+// rows with all of its loads in flight before any is summed, lane groups
+// are folded with shuffles and the 4 warps through shared memory. The
 // per-column summation order is fixed (deterministic).
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int64_t total_blocks,
                      float* __restrict__ cent) {
-    constexpr int L = D / 8, G = 32 / L, U = 8;
-    const int64_t wb = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (wb >= total_blocks) return;
-    const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
+    constexpr int L = D / 8, G = 32 / L, U = 8, W = 4;
+    __shared__ float part[W][D];
+    const int64_t wb = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
     const int n_blocks = (int)((N + B - 1) / B);
     const int64_t h = wb / n_blocks;
     const int j = (int)(wb - h * n_blocks);
@@ -113,11 +114,11 @@ centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int6
     const int len = (int)min64(B, N - t0);
     const uint4* base = reinterpret_cast<const uint4*>(K + (h * N + t0) * D) + sub;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r0 = grp; r0 < len; r0 += U * G) {
+    for (int r0 = warp * G + grp; r0 < len; r0 += U * W * G) {
         uint4 raw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int r = r0 + u * G;
+            const int r = r0 + u * W * G;
             raw[u] = (r < len) ? __ldg(base + (int64_t)r * L) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
@@ -135,11 +136,13 @@ centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int6
     for (int o = L; o < 32; o <<= 1)
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
-    if (grp == 0) {
-        const float inv = 1.f / (float)len;
-        float4* dst = reinterpret_cast<float4*>(cent + wb * D + sub * 8);
-        dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-        dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    if (grp == 0)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) part[warp][sub * 8 + c] = acc[c];
+    __syncthreads();
+    if (threadIdx.x < D) {
+        const float sum = (part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]);
+        cent[wb * D + threadIdx.x] = sum / (float)len;
     }
 }
 
@@ -238,13 +241,12 @@ extern "C" int moba_centroids(const void* k, const float* conv_w, int conv_width
     StageTimer tm(T_CENTROID, (cudaStream_t)stream);
     if (conv_width == 0 && (head_dim == 64 || head_dim == 128)) {
         const int64_t total = bh * n_blocks;
-        const unsigned g = (unsigned)ceil_div(total, 8);
         if (head_dim == 64)
-            centroid_warp_kernel<64><<<g, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
-                                                                         block_size, total, centroids);
+            centroid_warp_kernel<64><<<(unsigned)total, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
+                                                                                      block_size, total, centroids);
         else
-            centroid_warp_kernel<128><<<g, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
-                                                                          block_size, total, centroids);
+            centroid_warp_kernel<128><<<(unsigned)total, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
+                                                                                       block_size, total, centroids);
         return check_launch("centroid_warp_kernel");
     }
     centroid_conv_kernel<<<grid, kCentThreads, smem, (cudaStream_t)stream>>>(

@@ -32,7 +32,7 @@ METRICS = [
     ("launch__shared_mem_per_block_dynamic", "dyn smem/block"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
 ]
-STAGE_OF = {"moba_bwd": "bwd", "moba_fwd": "fwd", "route_topk": "route", "combine": "combine",
+STAGE_OF = {"moba_bwd": "bwd", "moba_fwd": "fwd", "route_topk": "route", "combine": "combine", "bwd_preprocess": "bwd_pre", "varlen": "varlen",
             "centroid": "centroid"}
 
 
