@@ -17,7 +17,7 @@ from .core import ConfigError, PlanValidationError, RoutingPlan, ShapeError
 
 SUPPORTED_DP = (64, 128)
 MAX_TOP_K = 31
-MAX_BLOCK = 256
+MAX_BLOCK = 512
 
 
 def padded_dim(d: int) -> int:

@@ -908,7 +908,7 @@ extern "C" int moba_bwd_gqa(const void* q, const void* k, const void* v, const v
                             void* dv, void* workspace, size_t workspace_bytes, void* stream) {
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
     if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
-    if (block_size > 256 || width > 32) return MOBA_ERR_UNSUPPORTED;
+    if (block_size > 512 || width > 32) return MOBA_ERR_UNSUPPORTED;
     const bool det = deterministic != 0;
     if (det && row_pos == nullptr) return MOBA_ERR_PLAN;
     if (workspace_bytes < bwd_ws(bh, n_tokens, head_dim, block_size, width, det, kv_group)) return MOBA_ERR_WORKSPACE;

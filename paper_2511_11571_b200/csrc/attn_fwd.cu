@@ -695,11 +695,15 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 // warp instruction fetches 32/L partial rows; all rounds are issued before
 // any is consumed. The lane groups are then reduced with shuffles and the
 // first L lanes write the row (coalesced).
-template <int D, int WMAX>
+template <int D, int WMAX, int slabs>
 __global__ void __launch_bounds__(256)
 moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_lse,
                     const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t total_rows,
                     __nv_bfloat16* __restrict__ O, float* __restrict__ LSE) {
+    // a query's partials: (slot, slab) pairs, virtual slot v = slot * slabs + slab
+    // at partial position row_pos[slot] * slabs + slab (slabs = 1 unless the
+    // key blocks are longer than 128)
+    const int vwidth = width * slabs;
     constexpr int L = D / 8;               // lanes per partial row
     constexpr int G = 32 / L;              // partial rows per warp instruction
     constexpr int R = (WMAX + G - 1) / G;  // load rounds per query
@@ -711,20 +715,23 @@ moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __res
     int32_t p[QW];
 #pragma unroll
     for (int t = 0; t < QW; ++t)
-        p[t] = (lane < width && row0 + t < total_rows) ? __ldg(row_pos + (row0 + t) * width + lane) : -1;
+    {
+        const int32_t q = (lane < vwidth && row0 + t < total_rows) ? __ldg(row_pos + (row0 + t) * width + lane / slabs) : -1;
+        p[t] = q >= 0 ? q * slabs + lane % slabs : -1;
+    }
     float ls[QW];
     uint4 raw[QW][R];
     int32_t pr[QW][R];
 #pragma unroll
     for (int t = 0; t < QW; ++t) {
         const int64_t h = (row0 + t) / N;
-        ls[t] = (p[t] >= 0) ? __ldg(part_lse + h * N * width + p[t]) : -INFINITY;
-        const uint4* base = reinterpret_cast<const uint4*>(part_o + h * N * width * D) + sub;
+        ls[t] = (p[t] >= 0) ? __ldg(part_lse + h * N * vwidth + p[t]) : -INFINITY;
+        const uint4* base = reinterpret_cast<const uint4*>(part_o + h * N * vwidth * D) + sub;
         const int32_t p0 = max(__shfl_sync(0xffffffffu, p[t], 0), 0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             pr[t][r] = __shfl_sync(0xffffffffu, p[t], (r * G + grp) & 31);
-            if (r * G + grp >= width) pr[t][r] = -1;
+            if (r * G + grp >= vwidth) pr[t][r] = -1;
             raw[t][r] = __ldg(base + (int64_t)(pr[t][r] >= 0 ? pr[t][r] : p0) * L);
         }
     }
@@ -767,17 +774,26 @@ moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __res
 
 template <int D>
 static void launch_combine(const void* part_o, const float* part_lse, const int32_t* row_pos, int64_t N, int width,
-                           int64_t rows, void* out, float* lse, cudaStream_t s) {
+                           int64_t rows, void* out, float* lse, cudaStream_t s, int slabs = 1) {
     const unsigned grid = (unsigned)ceil_div(rows, 8 * 2);
     auto po = (const __nv_bfloat16*)part_o;
     auto o = (__nv_bfloat16*)out;
-#define MOBA_COMBINE(W) moba_combine_kernel<D, W><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, rows, o, lse)
-    if (width <= 4) MOBA_COMBINE(4);
-    else if (width <= 8) MOBA_COMBINE(8);
-    else if (width <= 12) MOBA_COMBINE(12);
-    else if (width <= 16) MOBA_COMBINE(16);
-    else if (width <= 24) MOBA_COMBINE(24);
-    else MOBA_COMBINE(32);
+#define MOBA_COMBINE(W, S) moba_combine_kernel<D, W, S><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, rows, o, lse)
+#define MOBA_COMBINE_W(S)                                \
+    do {                                                 \
+        const int vw = width * (S);                      \
+        if (vw <= 4) MOBA_COMBINE(4, S);                 \
+        else if (vw <= 8) MOBA_COMBINE(8, S);            \
+        else if (vw <= 12) MOBA_COMBINE(12, S);          \
+        else if (vw <= 16) MOBA_COMBINE(16, S);          \
+        else if (vw <= 24) MOBA_COMBINE(24, S);          \
+        else MOBA_COMBINE(32, S);                        \
+    } while (0)
+    if (slabs == 1) MOBA_COMBINE_W(1);
+    else if (slabs == 2) MOBA_COMBINE_W(2);
+    else if (slabs == 3) MOBA_COMBINE_W(3);
+    else MOBA_COMBINE_W(4);
+#undef MOBA_COMBINE_W
 #undef MOBA_COMBINE
 }
 
@@ -785,8 +801,8 @@ static void launch_combine(const void* part_o, const float* part_lse, const int3
 // One thread per (head, block): exclusive scan of tile counts in a single
 // CTA, then each (head, block) writes its items.
 __global__ void __launch_bounds__(1024)
-fwd_items_scan_kernel(const int32_t* __restrict__ counts, int64_t total, int bm, int32_t* __restrict__ item_off,
-                      int32_t* __restrict__ n_items) {
+fwd_items_scan_kernel(const int32_t* __restrict__ counts, int64_t total, int bm, int mult,
+                      int32_t* __restrict__ item_off, int32_t* __restrict__ n_items) {
     __shared__ int32_t warp_tot[32];
     __shared__ int32_t carry;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -794,7 +810,7 @@ fwd_items_scan_kernel(const int32_t* __restrict__ counts, int64_t total, int bm,
     __syncthreads();
     for (int64_t b0 = 0; b0 < total; b0 += 1024) {
         int64_t b = b0 + threadIdx.x;
-        int32_t v = (b < total) ? (counts[b] + bm - 1) / bm : 0;
+        int32_t v = (b < total) ? (counts[b] + bm - 1) / bm * mult : 0;
         int32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -842,10 +858,14 @@ struct FwdWs {
     size_t part_o, part_lse, item_off, n_items, items, total;
 };
 
+// key-block slabs of the ping-pong forward: blocks longer than 128 keys are
+// processed as ceil(B / 128) slabs, each with its own partial
+static int fwd_slabs(int B) { return (int)ceil_div(B, 128); }
+
 static FwdWs fwd_ws_layout(int64_t bh, int64_t N, int D, int B, int width) {
     FwdWs w;
     int64_t n = ceil_div(N, B);
-    int64_t E = N * width;
+    int64_t E = N * width * fwd_slabs(B);
     size_t off = 0;
     w.part_o = off;
     off = align_up(off + (size_t)bh * E * D * 2, 256);
@@ -856,7 +876,8 @@ static FwdWs fwd_ws_layout(int64_t bh, int64_t N, int D, int B, int width) {
     w.n_items = off;
     off = align_up(off + 4, 256);
     w.items = off;
-    off = align_up(off + (size_t)bh * (ceil_div(E, kFwdBM) + n) * std::max(sizeof(FwdItem), fwd_ts_item_bytes()), 256);
+    off = align_up(off + (size_t)bh * (ceil_div(E, kFwdBM) + n * fwd_slabs(B)) *
+                             std::max(sizeof(FwdItem), fwd_ts_item_bytes()), 256);
     w.total = off;
     return w;
 }
@@ -866,7 +887,7 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int k
                   const int32_t* flat, const void* items, const int32_t* item_lo, const int32_t* item_hi,
                   float scale_log2, void* part_o, float* part_lse, cudaStream_t s);
 void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int32_t* item_off, int64_t total,
-                       void* items, cudaStream_t s);
+                       int slabs, void* items, cudaStream_t s);
 size_t fwd_ts_item_bytes();
 
 template <int D>
@@ -881,12 +902,13 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     FwdItem* items = (FwdItem*)(ws + L.items);
     const char* impl = std::getenv("MOBA_FWD_IMPL");
     const bool use_mma = impl != nullptr && impl[0] == 'm';
-    const bool use_ts = ceil_div(B, 16) * 16 <= 128 && (impl == nullptr || impl[0] == 't');
+    const int S = fwd_slabs(B);
+    const bool use_ts = (impl == nullptr || impl[0] == 't') && width * S <= 32;
     // GQA (kv_group > 1) is wired into the default kernels (ping-pong ts for
     // B <= 128, simple tcgen05 above); the legacy variants are MHA only
     if (kv_group > 1 && (use_mma || (!use_ts && ceil_div(B, 16) * 16 <= 128))) return MOBA_ERR_UNSUPPORTED;
     const int bm = use_mma ? kFwdBM : kTcM;
-    fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, bm, item_off, n_items);
+    fwd_items_scan_kernel<<<1, 1024, 0, s>>>(counts, total, bm, use_ts ? S : 1, item_off, n_items);
     if (!use_ts) fwd_items_fill_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, item_off, total, bm, items);
     int st = check_launch("fwd_items", use_ts ? 1 : 2);
     if (st) return st;
@@ -894,10 +916,10 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
     if (use_ts) {
         // heads in chunks whose partials (<= 48 MB) stay in L2 until the
         // chunk's combine reads them back
-        fwd_ts_fill_items(counts, offsets, item_off, total, items, s);
+        fwd_ts_fill_items(counts, offsets, item_off, total, S, items, s);
         st = check_launch("fwd_ts_items_kernel");
         if (st) return st;
-        const int64_t per_head = N * width * (int64_t)D * 2;
+        const int64_t per_head = N * width * (int64_t)S * D * 2;
         // (measured: smaller fwd launches cost more in pipeline ramp-up than the
         // combine saves, so by default all heads form one chunk)
         const char* chunk_env = std::getenv("MOBA_FWD_CHUNK_MB");
@@ -911,9 +933,9 @@ static int launch_fwd(const void* q, const void* k, const void* v, int64_t bh, i
                                   (float*)(ws + L.part_lse), s);
             if (st) return st;
             StageTimer tm(T_COMBINE, s);
-            launch_combine<D>(ws + L.part_o + h0 * N * width * D * 2, (const float*)(ws + L.part_lse) + h0 * N * width,
-                              row_pos + h0 * N * width, N, width, (h1 - h0) * N, (uint8_t*)out + h0 * N * D * 2,
-                              lse + h0 * N, s);
+            launch_combine<D>(ws + L.part_o + h0 * N * width * S * D * 2,
+                              (const float*)(ws + L.part_lse) + h0 * N * width * S, row_pos + h0 * N * width, N, width,
+                              (h1 - h0) * N, (uint8_t*)out + h0 * N * D * 2, lse + h0 * N, s, S);
             st = check_launch("moba_combine_kernel");
             if (st) return st;
         }
@@ -994,7 +1016,7 @@ extern "C" int moba_fwd_gqa(const void* q, const void* k, const void* v, int64_t
                             void* workspace, size_t workspace_bytes, void* stream) {
     if (bh < 1 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
     if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
-    if (width > 32 || block_size > 256) return MOBA_ERR_UNSUPPORTED;
+    if (width > 32 || block_size > 512) return MOBA_ERR_UNSUPPORTED;
     if (n_tokens * width >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
     FwdWs L = fwd_ws_layout(bh, n_tokens, head_dim, block_size, width);
     if (workspace_bytes < L.total) return MOBA_ERR_WORKSPACE;

@@ -86,6 +86,13 @@ MOBA_DEV void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, 
         : "memory");
 }
 
+// 3-D tiled store {c0, c1, c2} of an SW128 box from smem (bulk-group completion)
+MOBA_DEV void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(src)
+                 : "memory");
+}
+
 MOBA_DEV Item load_item(const Item* p) {
     int4 v = __ldg(reinterpret_cast<const int4*>(p));
     return Item{v.x, v.y, v.z, v.w};
@@ -95,7 +102,7 @@ MOBA_DEV Item load_item(const Item* p) {
 template <int D, int NCH>
 __global__ void __launch_bounds__(kThreads, 1)
 moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width, int kv_group,
+                   const __grid_constant__ CUtensorMap tm_v, int64_t N, int B, int BP, int width, int kv_group, int slabs,
                    const int32_t* __restrict__ flat, const Item* __restrict__ items,
                    const int32_t* __restrict__ item_lo, const int32_t* __restrict__ item_hi, float scale_log2,
                    __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse,
@@ -180,8 +187,10 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 const Item nxt = (li + 1 < n_local) ? load_item(my_items + li + 1) : cur;
                 const int64_t h = cur.hj / n_blocks;
                 const int j = cur.hj - (int)h * n_blocks;
-                if (cur.hj != prev_hj) {
-                    prev_hj = cur.hj;
+                const int kvkey = cur.hj * slabs + cur.pad;          // (block, 128-key slab)
+                const int krow = j * B + cur.pad * kM;
+                if (kvkey != prev_hj) {
+                    prev_hj = kvkey;
                     ++kv_uses;
                     if (pw == 0 && lane == 0) {
                         const int ks = kv_uses % C::KVS;
@@ -192,8 +201,8 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                         for (int sl = 0; sl < SL; ++sl) {
                             // GQA: query head h reads K/V head h / kv_group
                             const int hk = (int)(h / kv_group);
-                            tma_load_3d(kb + sl * BP * 128, &tm_k, sl * 64, j * B, hk, &bars->kv_full[ks]);
-                            tma_load_3d(kb + kv_bytes + sl * BP * 128, &tm_v, sl * 64, j * B, hk,
+                            tma_load_3d(kb + sl * BP * 128, &tm_k, sl * 64, krow, hk, &bars->kv_full[ks]);
+                            tma_load_3d(kb + kv_bytes + sl * BP * 128, &tm_v, sl * 64, krow, hk,
                                         &bars->kv_full[ks]);
                         }
                     }
@@ -236,15 +245,16 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
             int s_hj = -1, s_kv = -1;
             int kv_of[4] = {0, 0, 0, 0};
             // block ids of items li, li+1, li+2 (loaded two issues ahead)
-            int hj0 = my_items[0].hj;
-            int hj1 = n_local > 1 ? my_items[1].hj : -1;
-            int hj2 = n_local > 2 ? my_items[2].hj : -1;
+            auto kvkey = [&](int li) { return my_items[li].hj * slabs + my_items[li].pad; };
+            int hj0 = kvkey(0);
+            int hj1 = n_local > 1 ? kvkey(1) : -1;
+            int hj2 = n_local > 2 ? kvkey(2) : -1;
             auto issue_s = [&](int li) {
                 const int hj = hj0;
                 const bool last = hj1 != hj;
                 hj0 = hj1;
                 hj1 = hj2;
-                hj2 = (li + 3 < n_local) ? my_items[li + 3].hj : -1;
+                hj2 = (li + 3 < n_local) ? kvkey(li + 3) : -1;
                 if (hj != s_hj) {
                     s_hj = hj;
                     ++s_kv;
@@ -318,7 +328,8 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 const Item cur = nxt;
                 if (li + 2 < n_local) nxt = load_item(my_items + li + 2);
                 const int64_t h = cur.hj / n_blocks;
-                const int64_t k0 = (int64_t)(cur.hj - (int)h * n_blocks) * B;
+                const int64_t k0 = (int64_t)(cur.hj - (int)h * n_blocks) * B + (int64_t)cur.pad * kM;   // slab start
+                const int64_t slab_len = min64(min64((int64_t)B - (int64_t)cur.pad * kM, (int64_t)kM), N - k0);
                 const bool live = row < cur.rows;
                 const int qs = li % QS;
                 if (quad == 0) TR(li, 7);
@@ -331,7 +342,7 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 // visible keys of this row: columns [0, lim); columns
                 // [lim, NC) are masked (past the block end, token-causal in
                 // the own block, or never written by the MMA)
-                const int lim = live ? (int)min64(min64((int64_t)B, N - k0), (int64_t)q - k0 + 1) : 0;
+                const int lim = live ? (int)max64(0, min64(slab_len, (int64_t)q - k0 + 1)) : 0;
                 const bool masked = lim < NC;
                 float sv[NC];
 #pragma unroll
@@ -387,8 +398,8 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 // epilogue of li has read them before S(li + 4) can exist)
                 {
                     const uint32_t st = sbase + oST + ((li & 3) * kM + row) * 8;
-                    asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(st), "f"(1.f / l),
-                                 "f"((msl + __log2f(l)) * kLn2)
+                    asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(st), "f"(l > 0.f ? 1.f / l : 0.f),
+                                 "f"(l > 0.f ? (msl + __log2f(l)) * kLn2 : -INFINITY)
                                  : "memory");
                 }
                 tmem_st_wait();
@@ -415,7 +426,8 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 const Item cur = nxt;
                 if (li + 1 < n_local) nxt = load_item(my_items + li + 1);
                 const int b = li & 1;
-                const int64_t pb = (int64_t)(cur.hj / n_blocks) * N * width + cur.fl + row;
+                // partial of (flat position p, slab) at p * slabs + slab
+                const int64_t pb = ((int64_t)(cur.hj / n_blocks) * N * width + cur.fl + row) * slabs + cur.pad;
                 const bool live = row < cur.rows;
                 const bool full_warp = 32 * quad + 32 <= cur.rows;
                 const uint32_t obuf = tmem + C::kOCol + b * D + lane_off;
@@ -466,7 +478,7 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            tma_store_2d(&tm_po, stg, sl * 64, (int)(pb - lane));
+                            tma_store_3d(&tm_po, stg, sl * 64, cur.pad, (int)((pb - cur.pad) / slabs - lane));
                             bulk_commit();
                         }
                     }
@@ -486,26 +498,31 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
 
 // one thread per (head, block): its tiles' item records, at item_off[hj]
 __global__ void fwd_ts_items_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
-                                    const int32_t* __restrict__ item_off, int64_t total, Item* __restrict__ items) {
+                                    const int32_t* __restrict__ item_off, int64_t total, int slabs,
+                                    Item* __restrict__ items) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= total) return;
     const int cnt = counts[b], off = offsets[b];
     Item* dst = items + item_off[b];
-    for (int t = 0; t * kM < cnt; ++t) dst[t] = Item{(int32_t)b, off + t * kM, min(kM, cnt - t * kM), 0};
+    const int tiles = (cnt + kM - 1) / kM;
+    for (int sl = 0; sl < slabs; ++sl)
+        for (int t = 0; t < tiles; ++t) dst[sl * tiles + t] = Item{(int32_t)b, off + t * kM, min(kM, cnt - t * kM), sl};
 }
 
 }  // namespace fwdts
 
 bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t heads, uint64_t rows, uint32_t cols,
                        uint32_t box_rows);
+bool make_tmap_bf16_3d_box(CUtensorMap* map, const void* base, uint64_t outer, uint64_t mid, uint32_t cols,
+                           uint32_t box_mid, uint32_t box_outer);
 
 size_t fwd_ts_item_bytes() { return sizeof(fwdts::Item); }
 
 // item records for every (head, block): item_off = exclusive scan of the
 // per-(head, block) counts of 128-row tiles
 void fwd_ts_fill_items(const int32_t* counts, const int32_t* offsets, const int32_t* item_off, int64_t total,
-                       void* items, cudaStream_t s) {
-    fwdts::fwd_ts_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, offsets, item_off, total,
+                       int slabs, void* items, cudaStream_t s) {
+    fwdts::fwd_ts_items_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(counts, offsets, item_off, total, slabs,
                                                                              (fwdts::Item*)items);
 }
 
@@ -516,14 +533,16 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int k
                   const int32_t* flat, const void* items, const int32_t* item_lo, const int32_t* item_hi,
                   float scale_log2, void* part_o, float* part_lse, cudaStream_t s) {
     using namespace fwdts;
-    const int BP = (int)ceil_div(B, 16) * 16;
-    if (BP > 128) return MOBA_ERR_UNSUPPORTED;
+    const int slabs = (int)ceil_div(B, kM);          // keys of a block in slabs of <= 128
+    const int BP = (int)ceil_div(std::min(B, kM), 16) * 16;
     CUtensorMap tm_k, tm_v;
     if (!make_tmap_bf16_3d(&tm_k, k, (uint64_t)(bh / kv_group), (uint64_t)N, D, BP) ||
         !make_tmap_bf16_3d(&tm_v, v, (uint64_t)(bh / kv_group), (uint64_t)N, D, BP))
         return MOBA_ERR_CUDA;
     CUtensorMap tm_po;
-    if (!make_tmap_bf16(&tm_po, part_o, (uint64_t)(bh * N * width), D, 32)) return MOBA_ERR_CUDA;
+    // partials [bh * N * width][slabs][D]: 3-D map, box {64, 1 slab, 32 positions}
+    if (!make_tmap_bf16_3d_box(&tm_po, part_o, (uint64_t)(bh * N * width), (uint64_t)slabs, D, 1, 32))
+        return MOBA_ERR_CUDA;
     const size_t smem = 1024 + (size_t)Cfg<D>::QS * (Cfg<D>::kQBytes + kM * 4) + 2 * Cfg<D>::KVS * (size_t)BP * D * 2 + 4 * kStg +
                         4 * kM * 8 + sizeof(Bars);
     if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
@@ -540,7 +559,7 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int k
     if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
     {
         StageTimer tm(T_FWD, s);
-        kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, kv_group, flat,
+        kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, kv_group, slabs, flat,
                                           (const Item*)items, item_lo, item_hi, scale_log2, (__nv_bfloat16*)part_o,
                                           part_lse, tm_po, trace_path != nullptr ? trace : nullptr);
     }

@@ -132,6 +132,32 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t heads, uint6
     return true;
 }
 
+// bf16 [outer][mid][cols] with an SW128 box {64, box_mid, box_outer}
+bool make_tmap_bf16_3d_box(CUtensorMap* map, const void* base, uint64_t outer, uint64_t mid, uint32_t cols,
+                           uint32_t box_mid, uint32_t box_outer) {
+    CUtensorMap probe;
+    if (!make_tmap_bf16(&probe, base, outer * mid, cols, 1)) return false;   // resolves the driver entry point
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr)
+        return false;
+    EncodeTiledFn enc = (EncodeTiledFn)fn;
+    cuuint64_t dims[3] = {cols, mid, outer};
+    cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)cols * 2 * mid};
+    cuuint32_t box[3] = {64, box_mid, box_outer};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[96];
+        std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (3-D box) failed (%d)", (int)r);
+        set_last_error(buf);
+        return false;
+    }
+    return true;
+}
+
 }  // namespace moba
 
 extern "C" const char* moba_version(void) { return "moba_b200 0.1.0 sm_100a"; }

@@ -501,3 +501,24 @@ def test_cli_attend_tns1_vs_oracle(tmp_path):
     assert p["counts"] == plan.counts.tolist()
     assert p["offsets"] == plan.offsets.tolist()
     assert p["flat_queries"] == plan.flat_queries.tolist()
+
+
+@pytest.mark.parametrize("N,B,k,d", [(1536, 256, 4, 64), (2048, 512, 2, 64), (1000, 200, 3, 64), (1024, 256, 2, 128)])
+def test_large_blocks_vs_oracle(N, B, k, d):
+    """Key blocks longer than 128 keys (the paper's MoBA-256 / MoBA-512,
+    PAPER.md:317-320): the forward runs them as 128-key slabs with one
+    partial each; fwd + bwd against the oracle."""
+    gen = torch.Generator(device="cuda").manual_seed(B + k)
+    H = 2
+    q, kk, v, do = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(4))
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
+    out, lse = mb.moba_attn(qg, kg, vg, B, k, mode="fp32", deterministic=True, return_lse=True)
+    out.backward(do)
+    Qn, Kn, Vn, dOn = (t.double().cpu().numpy() for t in (q, kk, v, do))
+    for h in range(H):
+        plan = orc.build_plan(Qn[h], Kn[h], B, k)
+        O, L = orc.forward(Qn[h], Kn[h], Vn[h], plan, B)
+        dQ, dK, dV = orc.backward(Qn[h], Kn[h], Vn[h], O, dOn[h], L, plan, B)
+        for got, ref, nm in ((out[h], O, "O"), (lse[h], L, "LSE"), (qg.grad[h], dQ, "dQ"), (kg.grad[h], dK, "dK"),
+                             (vg.grad[h], dV, "dV")):
+            assert_close(got.detach().double().cpu().numpy(), ref, f"{nm}[{h}] B={B}")
