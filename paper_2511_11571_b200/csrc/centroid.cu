@@ -146,6 +146,71 @@ centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int6
     }
 }
 
+// Conv + centroids, vectorised (D in {64, 128}): one 128-thread CTA per
+// (head, block); a thread handles 8 channels of a row with 16-B loads of K
+// and its width-1 predecessors (L1 hits), writes K' (bf16) and accumulates
+// the unrounded fp32 K' for the centroid; fixed-order reduction.
+template <int D, int width>
+__global__ void __launch_bounds__(128)
+centroid_conv_vec_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W, int64_t N, int B,
+                         __nv_bfloat16* __restrict__ Kout, float* __restrict__ cent) {
+    constexpr int G = D / 8, RS = 128 / G;
+    __shared__ float red[RS][D];
+    const int j = blockIdx.x;
+    const int64_t h = blockIdx.y;
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int grp = threadIdx.x % G, rs = threadIdx.x / G;
+    const int64_t t0 = (int64_t)j * B;
+    const int len = (int)min64(B, N - t0);
+    const uint4* Kh = reinterpret_cast<const uint4*>(K + h * N * D);
+    uint4* Ko = reinterpret_cast<uint4*>(Kout + h * N * D);
+    float w[width][8];
+#pragma unroll
+    for (int l = 0; l < width; ++l)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) w[l][c] = W[l * D + grp * 8 + c];
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = rs; r < len; r += RS) {
+        const int64_t t = t0 + r;
+        uint4 raw[width];
+#pragma unroll
+        for (int l = 0; l < width; ++l) raw[l] = (t - l >= 0) ? __ldg(Kh + (t - l) * G + grp) : make_uint4(0, 0, 0, 0);
+        float x[8], a[8];
+#pragma unroll
+        for (int l = 0; l < width; ++l) {
+            const uint32_t v[4] = {raw[l].x, raw[l].y, raw[l].z, raw[l].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float2 f = unpack_bf16(v[c]);
+                if (l == 0) {
+                    x[2 * c] = f.x;
+                    x[2 * c + 1] = f.y;
+                    a[2 * c] = w[0][2 * c] * f.x;
+                    a[2 * c + 1] = w[0][2 * c + 1] * f.y;
+                } else {
+                    a[2 * c] = fmaf(w[l][2 * c], f.x, a[2 * c]);
+                    a[2 * c + 1] = fmaf(w[l][2 * c + 1], f.y, a[2 * c + 1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            x[c] = x[c] + a[c] * sigmoidf_acc(a[c]);      // K' = K + silu(conv(K)) (src/keyconv.py:77-78)
+            acc[c] += x[c];
+        }
+        Ko[t * G + grp] = make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]),
+                                     pack_bf16(x[6], x[7]));
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) red[rs][grp * 8 + c] = acc[c];
+    __syncthreads();
+    if (threadIdx.x < D) {
+        float sum = 0.f;
+        for (int g2 = 0; g2 < RS; ++g2) sum += red[g2][threadIdx.x];
+        cent[(h * n_blocks + j) * D + threadIdx.x] = sum / (float)len;
+    }
+}
+
 // ---------------------------------------------------------------- conv backward
 // key_conv_backward (src/keyconv.py:81-104). One CTA per (head, 64-row
 // chunk): g over the chunk plus a (width-1)-row lookahead in smem, then
@@ -206,6 +271,138 @@ conv_bwd_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W
     }
 }
 
+// Vectorised conv backward (D in {64, 128}): one CTA per (head, 64-row
+// chunk), 8 channels per thread with 16-B loads. K rows (with a width-1
+// halo on both sides) and dK' rows are staged in shared memory once; g, dK
+// and the per-CTA dW partials (fixed-order warp + CTA reductions) follow.
+template <int D, int width>
+__global__ void __launch_bounds__(256)
+conv_bwd_vec_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W,
+                    const __nv_bfloat16* __restrict__ dKc, int64_t N, __nv_bfloat16* __restrict__ dK,
+                    float* __restrict__ dw_part) {
+    constexpr int G = D / 8;                    // 8-channel groups
+    constexpr int RS = 256 / G;                 // row slots
+    constexpr int RK = kConvRows + 2 * (kMaxConv - 1);
+    constexpr int RG = kConvRows + kMaxConv - 1;
+    extern __shared__ __align__(16) uint8_t cb_smem[];
+    uint4* Ks = reinterpret_cast<uint4*>(cb_smem);                       // [RK][G] bf16x8
+    uint4* dks = Ks + RK * G;                                            // [RG][G] bf16x8
+    float4* gs = reinterpret_cast<float4*>(dks + RG * G);                // [RG][G][2] fp32x8
+    float* red = reinterpret_cast<float*>(gs + RG * G * 2);              // [8 warps][kMaxConv][D]
+    const int64_t h = blockIdx.y;
+    const int64_t t0 = (int64_t)blockIdx.x * kConvRows;
+    const int tid = threadIdx.x, grp = tid % G, rs = tid / G;
+    const int halo = width - 1;
+    const uint4* Kh = reinterpret_cast<const uint4*>(K + h * N * D);
+    const uint4* dKh = reinterpret_cast<const uint4*>(dKc + h * N * D);
+    // stage K rows [t0 - halo, t0 + 64 + halo) and dK' rows [t0, t0 + 64 + halo)
+    for (int e = tid; e < (kConvRows + 2 * halo) * G; e += 256) {
+        const int r = e / G, c = e % G;
+        const int64_t t = t0 - halo + r;
+        Ks[r * G + c] = (t >= 0 && t < N) ? __ldg(Kh + t * G + c) : make_uint4(0, 0, 0, 0);
+    }
+    for (int e = tid; e < (kConvRows + halo) * G; e += 256) {
+        const int r = e / G, c = e % G;
+        const int64_t t = t0 + r;
+        dks[r * G + c] = (t < N) ? __ldg(dKh + t * G + c) : make_uint4(0, 0, 0, 0);
+    }
+    float w[width][8];
+#pragma unroll
+    for (int l = 0; l < width; ++l)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) w[l][c] = W[l * D + grp * 8 + c];
+    __syncthreads();
+    auto unpack8 = [](uint4 u, float (&x)[8]) {
+        const uint32_t v[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float2 f = unpack_bf16(v[c]);
+            x[2 * c] = f.x;
+            x[2 * c + 1] = f.y;
+        }
+    };
+    // g_t = dK'_t * silu'(a_t), a_t = sum_l W[l] K[t-l] (src/keyconv.py:96)
+    for (int r = rs; r < kConvRows + halo; r += RS) {
+        const int64_t t = t0 + r;
+        float g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (t < N) {
+            float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int l = 0; l < width; ++l) {
+                float x[8];
+                unpack8(Ks[(r + halo - l) * G + grp], x);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) a[c] = fmaf(w[l][c], x[c], a[c]);
+            }
+            float dk[8];
+            unpack8(dks[r * G + grp], dk);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float sg = sigmoidf_acc(a[c]);
+                g[c] = dk[c] * (sg * (1.f + a[c] * (1.f - sg)));
+            }
+        }
+        gs[(r * G + grp) * 2] = make_float4(g[0], g[1], g[2], g[3]);
+        gs[(r * G + grp) * 2 + 1] = make_float4(g[4], g[5], g[6], g[7]);
+    }
+    __syncthreads();
+    // dK_t = dK'_t + sum_l W[l] g_{t+l};  dW[l] += g_t K_{t-l}  (src/keyconv.py:97-103)
+    float dwl[width][8];
+#pragma unroll
+    for (int l = 0; l < width; ++l)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dwl[l][c] = 0.f;
+    uint4* dKo = reinterpret_cast<uint4*>(dK + h * N * D);
+    for (int r = rs; r < kConvRows; r += RS) {
+        const int64_t t = t0 + r;
+        if (t >= N) break;
+        float v[8];
+        unpack8(dks[r * G + grp], v);
+        float gt[8];
+        {
+            const float4 a = gs[(r * G + grp) * 2], b = gs[(r * G + grp) * 2 + 1];
+            gt[0] = a.x; gt[1] = a.y; gt[2] = a.z; gt[3] = a.w; gt[4] = b.x; gt[5] = b.y; gt[6] = b.z; gt[7] = b.w;
+        }
+#pragma unroll
+        for (int l = 0; l < width; ++l) {
+            const float4 a = gs[((r + l) * G + grp) * 2], b = gs[((r + l) * G + grp) * 2 + 1];
+            const float gl[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            float x[8];
+            unpack8(Ks[(r + halo - l) * G + grp], x);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                v[c] = fmaf(w[l][c], gl[c], v[c]);
+                dwl[l][c] = fmaf(gt[c], x[c], dwl[l][c]);
+            }
+        }
+        dKo[t * G + grp] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                                      pack_bf16(v[6], v[7]));
+    }
+    // dW partial: lanes of a warp with the same channel group (xor over the
+    // row-slot bits), then the 8 warps in order
+#pragma unroll
+    for (int l = 0; l < width; ++l)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int o = G; o < 32; o <<= 1) dwl[l][c] += __shfl_xor_sync(0xffffffffu, dwl[l][c], o);
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane < G) {
+#pragma unroll
+        for (int l = 0; l < width; ++l)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) red[(warp * kMaxConv + l) * D + lane * 8 + c] = dwl[l][c];
+    }
+    __syncthreads();
+    const int64_t part = h * gridDim.x + blockIdx.x;
+    for (int e = tid; e < width * D; e += 256) {
+        const int l = e / D, c = e % D;
+        float acc = 0.f;
+        for (int wp = 0; wp < 8; ++wp) acc += red[(wp * kMaxConv + l) * D + c];
+        dw_part[(part * width + l) * D + c] = acc;
+    }
+}
+
 __global__ void conv_dw_reduce_kernel(const float* __restrict__ dw_part, int64_t n_parts, int width, int D,
                                       float* __restrict__ dw) {
     // one CTA per dW element, fixed-order strided sums + tree (deterministic)
@@ -249,6 +446,19 @@ extern "C" int moba_centroids(const void* k, const float* conv_w, int conv_width
                                                                                        block_size, total, centroids);
         return check_launch("centroid_warp_kernel");
     }
+    if (head_dim == 64 || head_dim == 128) {
+        using KernT = void (*)(const __nv_bfloat16*, const float*, int64_t, int, __nv_bfloat16*, float*);
+        static const KernT k64[kMaxConv] = {centroid_conv_vec_kernel<64, 1>, centroid_conv_vec_kernel<64, 2>,
+                                            centroid_conv_vec_kernel<64, 3>, centroid_conv_vec_kernel<64, 4>,
+                                            centroid_conv_vec_kernel<64, 5>};
+        static const KernT k128[kMaxConv] = {centroid_conv_vec_kernel<128, 1>, centroid_conv_vec_kernel<128, 2>,
+                                             centroid_conv_vec_kernel<128, 3>, centroid_conv_vec_kernel<128, 4>,
+                                             centroid_conv_vec_kernel<128, 5>};
+        const KernT kern = head_dim == 64 ? k64[conv_width - 1] : k128[conv_width - 1];
+        kern<<<grid, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, conv_w, n_tokens, block_size,
+                                                     (__nv_bfloat16*)k_conv_out, centroids);
+        return check_launch("centroid_conv_vec_kernel");
+    }
     centroid_conv_kernel<<<grid, kCentThreads, smem, (cudaStream_t)stream>>>(
         (const __nv_bfloat16*)k, conv_w, conv_width, n_tokens, head_dim, block_size,
         (__nv_bfloat16*)k_conv_out, centroids);
@@ -275,9 +485,27 @@ extern "C" int moba_conv_bwd(const void* k, const float* conv_w, int conv_width,
     }
     cudaStream_t s = (cudaStream_t)stream;
     StageTimer tm(T_CONV_BWD, s);
-    conv_bwd_kernel<<<grid, threads, smem, s>>>((const __nv_bfloat16*)k, conv_w, conv_width,
-                                            (const __nv_bfloat16*)dk_conv, n_tokens, head_dim,
-                                            (__nv_bfloat16*)dk, (float*)workspace);
+    if (head_dim == 64 || head_dim == 128) {
+        const int G = head_dim / 8;
+        const size_t vsmem = (size_t)(kConvRows + 2 * (kMaxConv - 1)) * G * 16 + (size_t)(kConvRows + kMaxConv - 1) * G * 16 +
+                             (size_t)(kConvRows + kMaxConv - 1) * G * 32 + (size_t)8 * kMaxConv * head_dim * 4;
+        using KernT = void (*)(const __nv_bfloat16*, const float*, const __nv_bfloat16*, int64_t, __nv_bfloat16*,
+                               float*);
+        static const KernT k64[kMaxConv] = {conv_bwd_vec_kernel<64, 1>, conv_bwd_vec_kernel<64, 2>,
+                                            conv_bwd_vec_kernel<64, 3>, conv_bwd_vec_kernel<64, 4>,
+                                            conv_bwd_vec_kernel<64, 5>};
+        static const KernT k128[kMaxConv] = {conv_bwd_vec_kernel<128, 1>, conv_bwd_vec_kernel<128, 2>,
+                                             conv_bwd_vec_kernel<128, 3>, conv_bwd_vec_kernel<128, 4>,
+                                             conv_bwd_vec_kernel<128, 5>};
+        const KernT kern = head_dim == 64 ? k64[conv_width - 1] : k128[conv_width - 1];
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem);
+        kern<<<grid, 256, vsmem, s>>>((const __nv_bfloat16*)k, conv_w, (const __nv_bfloat16*)dk_conv, n_tokens,
+                                      (__nv_bfloat16*)dk, (float*)workspace);
+    } else {
+        conv_bwd_kernel<<<grid, threads, smem, s>>>((const __nv_bfloat16*)k, conv_w, conv_width,
+                                                (const __nv_bfloat16*)dk_conv, n_tokens, head_dim,
+                                                (__nv_bfloat16*)dk, (float*)workspace);
+    }
     int st = check_launch("conv_bwd_kernel");
     if (st) return st;
     int e = conv_width * head_dim;
