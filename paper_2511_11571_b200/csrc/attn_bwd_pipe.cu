@@ -48,6 +48,7 @@ constexpr uint32_t kTile = 128 * 64 * 2;     // one 128 x 64 bf16 SW128 tile (16
 constexpr uint32_t cS0 = 0, cY = 256, cDV = 384, cDK = 448;
 constexpr uint32_t kStgRow = 32 * 4 + 16;    // half-row dQ staging (fp32) + pad
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr bool kBwdPolyExp = false;  // MUFU offload for 1 in 4 phase-A exponentials: measured slower (latency bound)
 
 struct Bars {
     uint64_t ring_full[kRing], ring_empty[kRing];
@@ -392,7 +393,9 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                         }
                     } else {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) sv[i + u] = fast_exp2(fmaf(sv[i + u], sl2, -l4[u]));
+                        for (int u = 0; u < 4; ++u)
+                            sv[i + u] = (kBwdPolyExp && u == 3) ? poly_exp2(fmaf(sv[i + u], sl2, -l4[u]))
+                                                                : fast_exp2(fmaf(sv[i + u], sl2, -l4[u]));
                     }
                 }
                 // sv now holds P (fp32, kept for phase B); bf16 pairs go to TMEM
