@@ -410,7 +410,7 @@ MOBA_DEV void select_chunk16(const float* sv, int j0, int lim, float (&ts)[KMAX]
 template <int D, int KMAX>
 __global__ void __launch_bounds__(kRt2Threads)
 route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
-                      int B, int top_k, int64_t split_rows, int kv_group, int32_t* __restrict__ topk) {
+                      int B, int top_k, int64_t split_rows, int kv_group, int c_bufs, int32_t* __restrict__ topk) {
     using namespace sm100;
     constexpr int SL = D / 64;
     constexpr uint32_t q_bytes = kRtM * D * 2;
@@ -419,7 +419,9 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* q_s = smem;
     uint8_t* c_s = q_s + q_bytes;                         // [2 buffers][3 terms][SL][64][128B]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(c_s + 2 * 3 * c_bytes);   // tma[2], mma[2]
+    // c_bufs = 1 when every CTA has a single 64-centroid chunk (N <= 64 B):
+    // no second C buffer, smaller footprint, three CTAs per SM
+    uint64_t* bars = reinterpret_cast<uint64_t*>(c_s + c_bufs * 3 * c_bytes);   // tma[2], mma[2]
     uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 4);
     float* sel_s = reinterpret_cast<float*>(tmem_ptr + 4);                   // [8 warps][16][32]
     int* sel_i = reinterpret_cast<int*>(sel_s + 8 * kRt2Buf * 32);          // [8 warps][16][32]
@@ -522,8 +524,8 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         tmem_dealloc(tmem, 2 * kRtN);
     }
     // merge the two halves' lists: half 1 publishes, half 0 merges and writes
-    float* ms = reinterpret_cast<float*>(c_s);                 // [KMAX][128] (C buffers are free now)
-    int* mi = reinterpret_cast<int*>(c_s + KMAX * kRtM * 4);
+    float* ms = reinterpret_cast<float*>(q_s);                 // [KMAX][128] (Q and C buffers are free now)
+    int* mi = reinterpret_cast<int*>(q_s + KMAX * kRtM * 4);
     if (half == 1) {
 #pragma unroll
         for (int u = 0; u < KMAX; ++u) {
@@ -892,11 +894,12 @@ static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N,
             kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, topk);
             return check_launch("route_topk_tc_kernel");
         }
-        static_assert(2 * 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the C buffers");
-        const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
+        static_assert(kRtM * 64 * 2 + 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the Q + C buffers");
+        const int c_bufs = ceil_div(n - 1, kRtN) <= 1 ? 1 : 2;
+        const size_t smem = 1024 + (size_t)kRtM * D * 2 + c_bufs * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
         auto kern = route_topk_tc2_kernel<D, KMAX>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, topk);
+        kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, c_bufs, topk);
         return check_launch("route_topk_tc2_kernel");
     }
     const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
