@@ -522,3 +522,54 @@ def test_large_blocks_vs_oracle(N, B, k, d):
         for got, ref, nm in ((out[h], O, "O"), (lse[h], L, "LSE"), (qg.grad[h], dQ, "dQ"), (kg.grad[h], dK, "dK"),
                              (vg.grad[h], dV, "dV")):
             assert_close(got.detach().double().cpu().numpy(), ref, f"{nm}[{h}] B={B}")
+
+
+def _sweep_cases(n=16, seed=2024):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        B = int(rng.choice([16, 32, 64, 96, 128, 192, 256, 512]))
+        N = int(rng.integers(B // 2 + 1, 6 * B + 1))
+        k = int(rng.integers(1, 9))
+        d = int(rng.choice([16, 32, 64, 100, 128]))
+        hkv = int(rng.choice([1, 2]))
+        G = int(rng.choice([1, 2, 3]))
+        conv = int(rng.choice([0, 0, 3, 5]))
+        cases.append((N, B, k, d, hkv, G, conv, bool(rng.integers(0, 2))))
+    return cases
+
+
+@pytest.mark.parametrize("N,B,k,d,hkv,G,conv,det", _sweep_cases())
+def test_randomized_sweep_vs_oracle(N, B, k, d, hkv, G, conv, det):
+    """Seeded random sweep over shapes (ragged N, B up to 512, d padded to
+    64/128, GQA groups, key conv, both dQ schedules): fp32 routing matches the
+    oracle's plan up to documented ties; O/LSE/dQ/dK/dV within tolerance."""
+    gen = torch.Generator(device="cuda").manual_seed(N * 7 + B)
+    hq = hkv * G
+    q, do = (torch.randn(hq, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    kk, v = (torch.randn(hkv, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
+    w = (torch.rand(conv, d, generator=gen, device="cuda") - 0.5) if conv else None
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
+    out, lse = mb.moba_attn(qg, kg, vg, B, k, conv_weight=w, mode="fp32", deterministic=det, return_lse=True)
+    out.backward(do)
+    Qn, Kn, Vn, dOn = (t.double().cpu().numpy() for t in (q, kk, v, do))
+    Wn = w.double().cpu().numpy() if conv else None
+    dK = np.zeros_like(Kn)
+    dV = np.zeros_like(Vn)
+    for h in range(hq):
+        hk = h // G
+        Kc = orc.key_conv_forward(Kn[hk], Wn) if conv else Kn[hk]
+        plan = orc.build_plan(Qn[h], Kc, B, k)
+        O, L = orc.forward(Qn[h], Kc, Vn[hk], plan, B)
+        dq, dkc, dv = orc.backward(Qn[h], Kc, Vn[hk], O, dOn[h], L, plan, B)
+        dk = orc.key_conv_backward(Kn[hk], Wn, dkc)[0] if conv else dkc
+        tag = f"h{h} N{N} B{B} k{k} d{d} G{G} conv{conv}"
+        assert_close(out[h].detach().double().cpu().numpy(), O, "O " + tag)
+        assert_close(lse[h].detach().double().cpu().numpy(), L, "LSE " + tag)
+        assert_close(qg.grad[h].double().cpu().numpy(), dq, "dQ " + tag)
+        dK[hk] += dk
+        dV[hk] += dv
+    # dK / dV of a K/V head sum G query heads' gradients (and are rounded to
+    # bf16 once at the larger magnitude): the absolute tolerance scales with G
+    assert_close(kg.grad.double().cpu().numpy(), dK, "dK", max_abs=2e-2 * G)
+    assert_close(vg.grad.double().cpu().numpy(), dV, "dV", max_abs=2e-2 * G)
