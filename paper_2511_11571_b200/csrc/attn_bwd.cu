@@ -14,6 +14,7 @@
 //
 // This is the legacy-MMA (mma.sync m16n8k16) path.
 #include "common.cuh"
+#include <type_traits>
 #include "sm100.cuh"
 #include <cstdlib>
 
@@ -253,9 +254,8 @@ moba_bwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __
 //              per-(query, block) partials); final dK, dV TMEM -> bf16
 // TMEM: S^T [0,128) dP^T [128,256) dV [256,256+D) dK [256+D,256+2D),
 //       dQ [256+2D, 256+3D) when it fits, else aliased onto S^T.
-__device__ long long* g_trace = nullptr;
 static long long* g_last_trace = nullptr;
-#define TRACE(slot) do { if (g_trace && blockIdx.x == 0 && lane == 0 && g < 64) g_trace[(g) * 16 + (slot)] = clock64(); } while (0)
+#define TRACE(slot) do { if (trace && blockIdx.x == 0 && lane == 0 && g < 64) trace[(g) * 16 + (slot)] = clock64(); } while (0)
 
 constexpr int kSmWarps = 8;                               // softmax-bwd warps
 constexpr int kPrWarps = 4;                               // producer (gather) warps
@@ -278,7 +278,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                    int kv_group, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                    const int32_t* __restrict__ flat, float scale, int qstages, int64_t n_items,
                    float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
-                   __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV) {
+                   __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, long long* __restrict__ trace) {
     using namespace sm100;
     constexpr int KT = 128;                     // keys per item (M of the key-side MMAs)
     constexpr int MQ = 128;                     // queries per tile
@@ -499,50 +499,61 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 const bool need_mask = rows_t < MQ || klen < KT || (int64_t)lds32i(id_a) < kb0 + KT - 1;
                 mbar_wait(&bars->p_empty, (g & 1) ^ 1);
                 if (warp == kSm0) TRACE(7);
+                // the mask test is a template argument, not a branch inside the
+                // unrolled loop (per-group branches serialise the loads and
+                // exponentials); padded rows carry id -1, dead key rows never pass
+                const int kmask = krow_ok ? (int)key : 0x7fffffff;
+                auto run_chunks = [&](auto mask_tag) {
+                    constexpr bool kMask = decltype(mask_tag)::value;
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
-                    const int c0 = half * 64 + c * 16;
-                    float sv[16], dpv[16];
-                    tmem_ld16(t_s + lane_off + c0, sv);
-                    tmem_ld16(t_dp + lane_off + c0, dpv);
-                    tmem_ld_wait();
-                    uint32_t pk[8], dk[8];
+                    for (int c = 0; c < 4; ++c) {
+                        const int c0 = half * 64 + c * 16;
+                        float sv[16], dpv[16];
+                        tmem_ld16(t_s + lane_off + c0, sv);
+                        tmem_ld16(t_dp + lane_off + c0, dpv);
+                        tmem_ld_wait();
+                        uint32_t pk[8], dk[8];
 #pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        const float4 lv = lds128f(l_a + (c0 + i) * 4);
-                        const float4 dv = lds128f(d_a + (c0 + i) * 4);
-                        const float la[4] = {lv.x, lv.y, lv.z, lv.w};
-                        const float da[4] = {dv.x, dv.y, dv.z, dv.w};
-                        float pv[4], dsv[4];
-                        if (need_mask) {
-                            const int4 iv = lds128i(id_a + (c0 + i) * 4);
-                            const int ia[4] = {iv.x, iv.y, iv.z, iv.w};
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 lv = lds128f(l_a + (c0 + i) * 4);
+                            const float4 dv = lds128f(d_a + (c0 + i) * 4);
+                            const float la[4] = {lv.x, lv.y, lv.z, lv.w};
+                            const float da[4] = {dv.x, dv.y, dv.z, dv.w};
+                            float pv[4], dsv[4];
+                            if constexpr (kMask) {
+                                const int4 iv = lds128i(id_a + (c0 + i) * 4);
+                                const int ia[4] = {iv.x, iv.y, iv.z, iv.w};
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const bool ok = krow_ok && ia[u] >= 0 && key <= (int64_t)ia[u];
-                                pv[u] = ok ? fast_exp2(fmaf(sv[i + u], sl2, -la[u])) : 0.f;
+                                for (int u = 0; u < 4; ++u) {
+                                    const float e = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
+                                    pv[u] = kmask <= ia[u] ? e : 0.f;
+                                }
+                            } else {
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) pv[u] = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
                             }
-                        } else {
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) pv[u] = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
+                            for (int u = 0; u < 4; ++u) dsv[u] = pv[u] * (dpv[i + u] - da[u]);
+                            pk[i >> 1] = pack_bf16(pv[0], pv[1]);
+                            pk[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
+                            dk[i >> 1] = pack_bf16(dsv[0], dsv[1]);
+                            dk[(i >> 1) + 1] = pack_bf16(dsv[2], dsv[3]);
                         }
+                        // P^T, dS^T (bf16 pairs) back into the S^T / dP^T columns just read
+                        // (A operands of the dV / dK MMAs); dS^T also to smem for dQ
+                        tmem_st8(t_s + lane_off + half * 64 + c * 8, pk);
+                        tmem_st8(t_dp + lane_off + half * 64 + c * 8, dk);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) dsv[u] = pv[u] * (dpv[i + u] - da[u]);
-                        pk[i >> 1] = pack_bf16(pv[0], pv[1]);
-                        pk[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
-                        dk[i >> 1] = pack_bf16(dsv[0], dsv[1]);
-                        dk[(i >> 1) + 1] = pack_bf16(dsv[2], dsv[3]);
+                        for (int gq = 0; gq < 2; ++gq) {
+                            const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
+                            sts128(ds_a + off, make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]));
+                        }
                     }
-                    // P^T, dS^T (bf16 pairs) back into the S^T / dP^T columns just read
-                    // (A operands of the dV / dK MMAs); dS^T also to smem for dQ
-                    tmem_st8(t_s + lane_off + half * 64 + c * 8, pk);
-                    tmem_st8(t_dp + lane_off + half * 64 + c * 8, dk);
-#pragma unroll
-                    for (int gq = 0; gq < 2; ++gq) {
-                        const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
-                        sts128(ds_a + off, make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]));
-                    }
-                }
+                };
+                if (need_mask)
+                    run_chunks(std::true_type{});
+                else
+                    run_chunks(std::false_type{});
                 tmem_st_wait();
                 tc_fence_before();
                 fence_proxy_async_smem();
@@ -841,16 +852,16 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         const int qstages = (fixed + 2 * stage_bytes <= 232448) ? 2 : 1;
         const size_t smem = fixed + qstages * stage_bytes;
         if (smem > 232448) return MOBA_ERR_UNSUPPORTED;
-        {
-            static long long* tr = nullptr;
-            if (std::getenv("MOBA_TRACE")) {
-                if (!tr) cudaMalloc(&tr, 64 * 16 * 8);
-                cudaMemsetAsync(tr, 0, 64 * 16 * 8, s);
-            }
-            long long* trp = std::getenv("MOBA_TRACE") ? tr : nullptr;
-            cudaMemcpyToSymbolAsync(g_trace, &trp, sizeof(trp), 0, cudaMemcpyHostToDevice, s);
-            g_last_trace = trp;
+        // debug timeline (MOBA_TRACE): a kernel argument, so a captured graph
+        // holds no host-memory copy node
+        static long long* tr = nullptr;
+        const bool tracing = std::getenv("MOBA_TRACE") != nullptr;
+        if (tracing) {
+            if (!tr) cudaMalloc(&tr, 64 * 16 * 8);
+            cudaMemsetAsync(tr, 0, 64 * 16 * 8, s);
         }
+        long long* trp = tracing ? tr : nullptr;
+        g_last_trace = trp;
         CUtensorMap tm_k, tm_v;
         if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh / kv_group * N), D, 128) ||
             !make_tmap_bf16(&tm_v, v, (uint64_t)(bh / kv_group * N), D, 128))
@@ -861,7 +872,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         const int grid = (int)std::min<int64_t>(n_items, kNumSMs);
         kern<<<grid, kBwdTcThreads, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, N, B,
                                                width, kv_group, counts, offsets, flat, scale, qstages, n_items, dq_acc,
-                                               dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
+                                               dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, trp);
         st = check_launch("moba_bwd_tc_kernel");
     }
     }
