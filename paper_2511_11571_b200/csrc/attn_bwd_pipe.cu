@@ -14,7 +14,7 @@
 //                                                 an SW128 smem tile (A of dQ)
 //   dV += P^T dO, dK += dS^T Q  (TS-MMAs, TMEM accumulators over the item)
 //   dQ(g)   = dS K           -> slot[64:128), drained by the epilogue warps
-//             with one bulk fp32 reduce-add per half row
+//             with one 256-B bulk fp32 reduce-add per row
 // S^T(g+1) runs on the tensor pipe while the softmax warps do phase A of g;
 // dP^T(g+1) is issued right behind the dV/dK/dQ MMAs of g (tcgen05.mma
 // executes in issue order, so Y and the slots are reused without waits).
@@ -46,7 +46,8 @@ constexpr int kRing = 8;                // item ring depth
 constexpr int kRingConsumers = (kPr - 1) + 1 + kSmN + kEpN;
 constexpr uint32_t kTile = 128 * 64 * 2;     // one 128 x 64 bf16 SW128 tile (16 KB)
 constexpr uint32_t cS0 = 0, cY = 256, cDV = 384, cDK = 448;
-constexpr uint32_t kStgRow = 32 * 4 + 16;    // half-row dQ staging (fp32) + pad
+constexpr uint32_t kStgRow = 64 * 4 + 16;    // full-row dQ staging (fp32) + pad
+constexpr uint32_t kStgRows = 16;            // staged rows per epilogue warp (two rounds of 16 lanes)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr bool kBwdPolyExp = false;  // MUFU offload for 1 in 4 phase-A exponentials: measured slower (latency bound)
 
@@ -54,7 +55,7 @@ struct Bars {
     uint64_t ring_full[kRing], ring_empty[kRing];
     uint64_t kv_full[2], kv_empty[2];
     uint64_t qd_full[kQSt], qd_empty[kQSt];
-    uint64_t s_full[2], dp_full, p_full;
+    uint64_t s_full[2], pa_full[2], dp_full, p_full;
     uint64_t dq_full[2], dq_empty[2];
     uint64_t dkv_full, dkv_empty;
     int ring[kRing];
@@ -66,8 +67,8 @@ constexpr uint32_t oKV = 0;                                  // [2][K | V]
 constexpr uint32_t oQD = oKV + 2 * 2 * kTile;                // [kQSt][Q | dO]
 constexpr uint32_t oDS = oQD + kQSt * 2 * kTile;             // dS^T [2 query slabs][128 keys][128 B]
 constexpr uint32_t oLDI = oDS + 2 * kTile;                   // [kQSt][L | D | id] x 128 x 4 B
-constexpr uint32_t oSTG = oLDI + kQSt * 3 * MQ * 4;          // dQ staging 128 x kStgRow
-constexpr uint32_t oBAR = oSTG + MQ * kStgRow;
+constexpr uint32_t oSTG = oLDI + kQSt * 3 * MQ * 4;          // dQ staging kEpN x kStgRows x kStgRow
+constexpr uint32_t oBAR = oSTG + kEpN * kStgRows * kStgRow;
 constexpr uint32_t kSmem = 1024 + oBAR + sizeof(Bars);
 
 struct Item {
@@ -139,6 +140,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
             mbar_init(&bars->kv_full[i], 1);
             mbar_init(&bars->kv_empty[i], 1);
             mbar_init(&bars->s_full[i], 1);
+            mbar_init(&bars->pa_full[i], kSmN);
             mbar_init(&bars->dq_full[i], 1);
             mbar_init(&bars->dq_empty[i], kEpN);
         }
@@ -285,25 +287,22 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
             TRB(g, 3);
             tc_fence_after();
             fence_proxy_async_smem();
-            if (lane == 0) {
-                const uint32_t kb = kv_addr(tl.kvs), qb = qd_addr(g % kQSt);
+            // warp-uniform issue (elect.sync in the asm) with descriptors
+            // advanced by constant offsets: a few instructions per MMA, which
+            // matters because this warp shares its issue slots with softmax
+            // and epilogue warps (K-major: +32 B per K16 step)
+            const uint64_t dk = desc_kmajor(kv_addr(tl.kvs), 0), dq = desc_kmajor(qd_addr(g % kQSt), 0);
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
-                    umma_bf16(tmem + cS0 + (g & 1) * 128, desc_kmajor(kb, kk * 16), desc_kmajor(qb, kk * 16),
-                              idesc_kq, kk > 0);
-                umma_commit(&bars->s_full[g & 1]);
-            }
-            __syncwarp();
+            for (int kk = 0; kk < D / 16; ++kk)
+                umma_bf16_w(tmem + cS0 + (g & 1) * 128, dk + 2 * kk, dq + 2 * kk, idesc_kq, kk > 0);
+            umma_commit_w(&bars->s_full[g & 1]);
         };
         auto issue_dp = [&](const Tile& tl, int g) {
-            if (lane == 0) {
-                const uint32_t vb = kv_addr(tl.kvs) + kTile, db = qd_addr(g % kQSt) + kTile;
+            const uint64_t dv = desc_kmajor(kv_addr(tl.kvs) + kTile, 0), ddo = desc_kmajor(qd_addr(g % kQSt) + kTile, 0);
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk)
-                    umma_bf16(tmem + cY, desc_kmajor(vb, kk * 16), desc_kmajor(db, kk * 16), idesc_kq, kk > 0);
-                umma_commit(&bars->dp_full);
-            }
-            __syncwarp();
+            for (int kk = 0; kk < D / 16; ++kk)
+                umma_bf16_w(tmem + cY, dv + 2 * kk, ddo + 2 * kk, idesc_kq, kk > 0);
+            umma_commit_w(&bars->dp_full);
         };
         Tile cur, nxt;
         bool have = next_tile(cur);
@@ -315,32 +314,38 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
         while (have) {
             const bool have_n = next_tile(nxt);
             if (have_n) issue_s(nxt, g + 1);
-            mbar_wait(&bars->p_full, g & 1);
+            // dV(g) needs only P(g): issued as soon as phase A has stored it,
+            // so it runs on the tensor pipe while the softmax does phase B
+            mbar_wait(&bars->pa_full[g & 1], (g >> 1) & 1);
             if (cur.first) mbar_wait(&bars->dkv_empty, (cur.kvu & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t slot = tmem + cS0 + (g & 1) * 128;
+            // MN-major operands: +16 rows x 128 B = 2 KB per K16 step
+            const uint64_t d_k = desc_mnmajor(kv_addr(cur.kvs), 0, KT * 128);
+            const uint64_t d_q = desc_mnmajor(qd_addr(g % kQSt), 0, MQ * 128);
+            const uint64_t d_do = desc_mnmajor(qd_addr(g % kQSt) + kTile, 0, MQ * 128);
+            const uint64_t d_ds = desc_mnmajor(sbase + oDS, 0, KT * 128);
+#pragma unroll
+            for (int kk = 0; kk < MQ / 16; ++kk)
+                umma_bf16_ts_w(tmem + cDV, slot + 8 * kk, d_do + 128 * kk, idesc_kd, !cur.first || kk > 0);
+            mbar_wait(&bars->p_full, g & 1);
             TRB(g, 4);
             tc_fence_after();
             fence_proxy_async_smem();
-            if (lane == 0) {
-                const uint32_t slot = tmem + cS0 + (g & 1) * 128;
-                const uint32_t kb = kv_addr(cur.kvs), qb = qd_addr(g % kQSt), db = qb + kTile;
+            // dK and dQ interleaved: two independent accumulation chains
 #pragma unroll
-                for (int kk = 0; kk < MQ / 16; ++kk) {
-                    const bool acc = !cur.first || kk > 0;
-                    umma_bf16_ts(tmem + cDV, slot + 8 * kk, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, acc);
-                    umma_bf16_ts(tmem + cDK, tmem + cY + 8 * kk, desc_mnmajor(qb, kk * 16, MQ * 128), idesc_kd, acc);
-                }
-#pragma unroll
-                for (int kk = 0; kk < KT / 16; ++kk)
-                    umma_bf16(slot + 64, desc_mnmajor(sbase + oDS, kk * 16, KT * 128),
-                              desc_mnmajor(kb, kk * 16, KT * 128), idesc_qd, kk > 0);
-                umma_commit(&bars->dq_full[g & 1]);
-                umma_commit(&bars->qd_empty[g % kQSt]);
-                if (cur.last) {
-                    umma_commit(&bars->dkv_full);
-                    umma_commit(&bars->kv_empty[cur.kvs]);
-                }
+            for (int kk = 0; kk < MQ / 16; ++kk) {
+                umma_bf16_ts_w(tmem + cDK, tmem + cY + 8 * kk, d_q + 128 * kk, idesc_kd, !cur.first || kk > 0);
+                umma_bf16_w(slot + 64, d_ds + 128 * kk, d_k + 128 * kk, idesc_qd, kk > 0);
             }
-            __syncwarp();
+            TRB(g, 13);
+            TRB(g, 14);
+            umma_commit_w(&bars->dq_full[g & 1]);
+            umma_commit_w(&bars->qd_empty[g % kQSt]);
+            if (cur.last) {
+                umma_commit_w(&bars->dkv_full);
+                umma_commit_w(&bars->kv_empty[cur.kvs]);
+            }
             TRB(g, 5);
             if (have_n) issue_dp(nxt, g + 1);
             cur = nxt;
@@ -416,6 +421,10 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(sv[2 * e], sv[2 * e + 1]);
                 named_bar(1 + quad, 64);        // both halves have read S^T from the slot
                 tmem_st32(slot + lane_off + 32 * half, pk);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->pa_full[g & 1]);
                 if (warp == kSm0) TRB(g, 8);
                 // ---- phase B
                 mbar_wait(&bars->dp_full, g & 1);
@@ -458,7 +467,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
         const int quad = warp & 3;
         const int row = 32 * quad + lane;
         const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
-        const uint32_t srow = sbase + oSTG + row * kStgRow;
+        const uint32_t srow = sbase + oSTG + (quad * kStgRows + (lane & 15)) * kStgRow;
         int g = 0, kv_use = 0;
         for (;;) {
             const int it = rr.next(bars, lane);
@@ -479,24 +488,33 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->dq_empty[g & 1]);
+                // one 256-B bulk op per row (fp32 reduce-add into dQ, or a
+                // store of the per-(query, block) partial when deterministic);
+                // the warp's 32 rows are staged 16 at a time. The bulk ops are
+                // per-thread (a single issuing thread serialises them) and
+                // each compiles to an elect/broadcast iteration, so fewer,
+                // larger ops is what shortens this loop.
                 const int64_t r_in = t * MQ + row;
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    bulk_wait_read0();                       // staging row free
+                for (int rr = 0; rr < 2; ++rr) {
+                    bulk_wait_read0();                       // the previous round's rows have been read
+                    __syncwarp();
+                    if ((lane >> 4) == rr) {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4)
-                        sts128(srow + i * 4, make_uint4(__float_as_uint(v[32 * hh + i]), __float_as_uint(v[32 * hh + i + 1]),
-                                                        __float_as_uint(v[32 * hh + i + 2]),
-                                                        __float_as_uint(v[32 * hh + i + 3])));
-                    fence_proxy_async_smem();
-                    if (qi >= 0) {
-                        if (dq_part != nullptr)
-                            bulk_store(dq_part + x.slab * part_stride + (x.fl_base + r_in) * D + 32 * hh, srow, 128);
-                        else
-                            bulk_reduce_add_f32(dq_acc + (x.h * N + qi) * D + 32 * hh, srow, 128);
+                        for (int i = 0; i < 64; i += 4)
+                            sts128(srow + i * 4, make_uint4(__float_as_uint(v[i]), __float_as_uint(v[i + 1]),
+                                                            __float_as_uint(v[i + 2]), __float_as_uint(v[i + 3])));
+                        fence_proxy_async_smem();
+                        if (qi >= 0) {
+                            if (dq_part != nullptr)
+                                bulk_store(dq_part + x.slab * part_stride + (x.fl_base + r_in) * D, srow, 256);
+                            else
+                                bulk_reduce_add_f32(dq_acc + (x.h * N + qi) * D, srow, 256);
+                        }
+                        bulk_commit();
                     }
-                    bulk_commit();
                 }
+                if (warp == kEp0) TRB(g, 12);
             }
             // dK (scaled), dV of the slab; zeros when no query attends the block
             const bool live = row < x.klen;
