@@ -382,15 +382,15 @@ def test_host_pipeline_matches_device_path(n_chunks, graphs):
         assert torch.equal(got, ref.detach().cpu()), nm
 
 
-@pytest.mark.parametrize("conv,d", [(False, 64), (True, 64), (False, 128)])
-def test_graphed_step_matches_eager(conv, d):
+@pytest.mark.parametrize("conv,d,B", [(False, 64, 128), (True, 64, 128), (False, 128, 128), (False, 64, 256)])
+def test_graphed_step_matches_eager(conv, d, B):
     """MobaGraphedStep (the whole fwd+bwd captured once, replayed) gives
     bitwise the eager results, also after the inputs change (a new plan).
     d = 128 runs the other backward kernel (its debug-trace pointer once went
     through a host-memory copy that a captured graph replayed from a stale
     stack address)."""
     gen = torch.Generator(device="cuda").manual_seed(5)
-    H, N, B, k = 3, 1536, 128, 4
+    H, N, k = 3, 1536, 4
     w = (torch.rand(3, d, generator=gen, device="cuda") - 0.5) if conv else None
     gs = mb.MobaGraphedStep((H, N, d), B, k, mode="tc", deterministic=True, conv_weight=w)
     for trial in range(2):
