@@ -450,7 +450,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--route-mode", choices=["fp32", "tc"], default="tc")
     ap.add_argument("--deterministic", action="store_true", help="deterministic dQ schedule")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="head chunks of the host-buffer pipeline")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="head chunks of the host-buffer pipeline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="headline from eager launches instead of a CUDA graph")
