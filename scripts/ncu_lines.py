@@ -1,12 +1,13 @@
 """Attribute ncu warp-stall samples to CUDA source lines (innermost line in
 the kernel's own .cu file, following 'inlined at' chains).
 
-usage: python scripts/ncu_lines.py <report.ncu-rep> <cubin> <kernel.cu> [top]
+usage: python scripts/ncu_lines.py <report.ncu-rep> <cubin> <kernel.cu> [top] [mangled function name]
 """
 import csv, io, re, subprocess, sys
 
 rep, cubin, cu = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+fun = sys.argv[5] if len(sys.argv) > 5 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -16,7 +17,13 @@ ia, iall = h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
 base = min(int(r[ia], 16) for r in data)
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 cur, off2line = None, {}
+in_fun = fun is None
 for ln in dis.splitlines():
+    if fun is not None and ln.lstrip().startswith(".text."):
+        in_fun = fun in ln
+        continue
+    if not in_fun:
+        continue
     if "//## File" in ln:
         # pick the first (file, line) pair on the line that is in our .cu
         pairs = re.findall(r'File "([^"]+)", line (\d+)', ln)
