@@ -454,7 +454,7 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             for (int sl = 0; sl < SL; ++sl)
                 tma_load_2d(smem_u32(q_s) + sl * kRtM * 128, &tm_q, sl * 64, (int)(h * N + r0), &bars[buf]);
         }
-        const uint32_t cb = smem_u32(c_s) + buf * 3 * c_bytes;
+        const uint32_t cb = smem_u32(c_s) + (c_bufs == 2 ? buf : 0) * 3 * c_bytes;
 #pragma unroll
         for (int term = 0; term < 3; ++term)
 #pragma unroll
@@ -466,7 +466,7 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         const int buf = c & 1;
         mbar_wait(&bars[buf], (c >> 1) & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(q_s), cb = smem_u32(c_s) + buf * 3 * c_bytes;
+        const uint32_t qa = smem_u32(q_s), cb = smem_u32(c_s) + (c_bufs == 2 ? buf : 0) * 3 * c_bytes;
         bool acc = false;
 #pragma unroll
         for (int term = 0; term < 3; ++term)
@@ -480,9 +480,14 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         umma_commit(&bars[2 + buf]);
     };
 
+    // c_bufs = 2: chunk c+2 is loaded while chunk c is selected and MMA(c+1)
+    // runs ahead. c_bufs = 1 (one centroid buffer, smaller footprint, one
+    // more CTA per SM): chunk c+1 is loaded while chunk c is selected and
+    // its MMA is issued at the top of the next iteration. TMA barrier and
+    // TMEM slot of chunk c are c & 1 either way.
     if (tid == 0 && n_chunks > 0) {
         load_chunk(0, 0);
-        if (n_chunks > 1) load_chunk(1, 1);
+        if (c_bufs == 2 && n_chunks > 1) load_chunk(1, 1);
         issue_mma(0);
     }
 
@@ -501,11 +506,16 @@ route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     }
     for (int c = 0; c < n_chunks; ++c) {
         const int buf = c & 1;
+        if (c_bufs == 1 && c > 0 && tid == 0) issue_mma(c);
         mbar_wait(&bars[2 + buf], (c >> 1) & 1);        // S(c) in TMEM, smem buffer free
         tc_fence_after();
         if (tid == 0) {
-            if (c + 1 < n_chunks) issue_mma(c + 1);
-            if (c + 2 < n_chunks) load_chunk(c + 2, buf);
+            if (c_bufs == 2) {
+                if (c + 1 < n_chunks) issue_mma(c + 1);
+                if (c + 2 < n_chunks) load_chunk(c + 2, buf);
+            } else if (c + 1 < n_chunks) {
+                load_chunk(c + 1, (c + 1) & 1);
+            }
         }
         const int j0 = c * kRtN + 32 * half;
         const int lim = (my_i < N) ? min(32, my_own - j0) : 0;   // strictly-past blocks only
@@ -895,7 +905,10 @@ static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N,
             return check_launch("route_topk_tc_kernel");
         }
         static_assert(kRtM * 64 * 2 + 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the Q + C buffers");
-        const int c_bufs = ceil_div(n - 1, kRtN) <= 1 ? 1 : 2;
+        // one centroid buffer (3 CTAs per SM instead of 2) unless
+        // MOBA_ROUTE_CBUFS=2: measured 64K route 0.99 -> 0.86 ms
+        static const int cb_env = std::getenv("MOBA_ROUTE_CBUFS") ? std::atoi(std::getenv("MOBA_ROUTE_CBUFS")) : 1;
+        const int c_bufs = ceil_div(n - 1, kRtN) <= 1 ? 1 : (cb_env == 2 ? 2 : 1);
         const size_t smem = 1024 + (size_t)kRtM * D * 2 + c_bufs * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
         auto kern = route_topk_tc2_kernel<D, KMAX>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
