@@ -689,6 +689,9 @@ moba_fwd_ws_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 }
 
 // ---------------------------------------------------------------- combine
+#ifndef MOBA_COMBINE_QW
+#define MOBA_COMBINE_QW 1   // one query per warp: fewer registers, more warps in flight (64K combine 0.78 -> 0.62 ms vs 2)
+#endif
 // One warp per query: merge its <= width partials (lse-weighted,
 // SoftmaxState.finalize over the query's blocks, src/attention.py:70-74).
 // A partial row (D bf16) is read by L = D/8 lanes with 16-B loads, so one
@@ -707,7 +710,7 @@ moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __res
     constexpr int L = D / 8;               // lanes per partial row
     constexpr int G = 32 / L;              // partial rows per warp instruction
     constexpr int R = (WMAX + G - 1) / G;  // load rounds per query
-    constexpr int QW = 2;                  // queries per warp, loads of both in flight together
+    constexpr int QW = MOBA_COMBINE_QW;    // queries per warp, loads of all in flight together
     const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * QW;
     const int lane = threadIdx.x & 31;
     if (row0 >= total_rows) return;
@@ -775,7 +778,7 @@ moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __res
 template <int D>
 static void launch_combine(const void* part_o, const float* part_lse, const int32_t* row_pos, int64_t N, int width,
                            int64_t rows, void* out, float* lse, cudaStream_t s, int slabs = 1) {
-    const unsigned grid = (unsigned)ceil_div(rows, 8 * 2);
+    const unsigned grid = (unsigned)ceil_div(rows, 8 * MOBA_COMBINE_QW);
     auto po = (const __nv_bfloat16*)part_o;
     auto o = (__nv_bfloat16*)out;
 #define MOBA_COMBINE(W, S) moba_combine_kernel<D, W, S><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, rows, o, lse)
