@@ -742,6 +742,67 @@ varlen_scatter_kernel(const int32_t* __restrict__ topk, int64_t N, int width, in
     for (int e = tid; e < nq * width; e += blockDim.x) rp[e] = rows_s[e];
 }
 
+// Same output as varlen_scatter_kernel with the chunk's queries split over
+// the CTA's 4 warps: each warp histograms its quarter of the rows, the
+// per-block cursors of warp w start after warps < w, and the 4 warps walk
+// their quarters concurrently (the single walking warp was the critical
+// path: 36 dependent steps per 128-query chunk).
+__global__ void __launch_bounds__(128)
+varlen_scatter4_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int n_blocks, int TQ,
+                       int n_chunks, const int32_t* __restrict__ cc, const int32_t* __restrict__ offsets,
+                       int32_t* __restrict__ flat, int32_t* __restrict__ row_pos) {
+    extern __shared__ int32_t vsm[];
+    int32_t* cursor = vsm;                   // [4][n_blocks]
+    int32_t* rows_s = vsm + 4 * n_blocks;    // [TQ * width]
+    const int64_t h = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t i0 = (int64_t)chunk * TQ;
+    const int nq = (int)(min64(i0 + TQ, N) - i0);
+    const int32_t* tk = topk + (h * N + i0) * width;
+    for (int e = tid; e < nq * width; e += blockDim.x) rows_s[e] = __ldg(tk + e);
+    for (int b = tid; b < 4 * n_blocks; b += blockDim.x) cursor[b] = 0;
+    __syncthreads();
+    const int q4 = (nq + 3) / 4;
+    const int e_lo = min(nq, warp * q4) * width, e_hi = min(nq, (warp + 1) * q4) * width;
+    int32_t* cur = cursor + warp * n_blocks;
+    for (int e = e_lo + lane; e < e_hi; e += 32) {
+        const int32_t b = rows_s[e];
+        if (b >= 0) atomicAdd(&cur[b], 1);
+    }
+    __syncthreads();
+    const int32_t* ccc = cc + (h * n_chunks + chunk) * (int64_t)n_blocks;
+    for (int b = tid; b < n_blocks; b += blockDim.x) {
+        int32_t run = offsets[h * n_blocks + b] + ccc[b];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int32_t c = cursor[w * n_blocks + b];
+            cursor[w * n_blocks + b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    int32_t* fl = flat + h * N * width;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
+        const int e = e0 + lane;
+        const int32_t b = (e < e_hi) ? rows_s[e] : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, b);
+        int32_t p = -1;
+        if (b >= 0) {
+            p = cur[b] + __popc(grp & lt);
+            fl[p] = (int32_t)(i0 + e / width);
+        }
+        __syncwarp();
+        if (b >= 0 && (grp & lt) == 0) cur[b] += __popc(grp);   // group leader advances the cursor
+        if (e < e_hi) rows_s[e] = p;
+        __syncwarp();
+    }
+    __syncthreads();
+    int32_t* rp = row_pos + (h * N + i0) * width;
+    for (int e = tid; e < nq * width; e += blockDim.x) rp[e] = rows_s[e];
+}
+
 // row_pos from an arbitrary (validated) plan: binary search of query i in
 // block b's ascending slice.
 __global__ void plan_row_pos_kernel(const int32_t* __restrict__ topk, const int32_t* __restrict__ counts,
@@ -870,7 +931,14 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     varlen_scan_kernel<<<(unsigned)bh, 1024, 0, s>>>(cc, g.n_blocks, g.n_chunks, counts, offsets);
     st = check_launch("varlen_scan_kernel");
     if (st) return st;
-    const size_t ssmem = hsmem + (size_t)g.TQ * width * sizeof(int32_t);
+    const size_t rsmem = (size_t)g.TQ * width * sizeof(int32_t);
+    const size_t ssmem4 = 4 * hsmem + rsmem;
+    if (ssmem4 <= 48 * 1024) {
+        varlen_scatter4_kernel<<<dim3(g.n_chunks, (unsigned)bh), 128, ssmem4, s>>>(
+            topk, N, width, g.n_blocks, g.TQ, g.n_chunks, cc, offsets, flat, row_pos);
+        return check_launch("varlen_scatter4_kernel");
+    }
+    const size_t ssmem = hsmem + rsmem;
     if (ssmem > 48 * 1024) {
         if (ssmem > 227 * 1024) return MOBA_ERR_UNSUPPORTED;
         cudaFuncSetAttribute(varlen_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
