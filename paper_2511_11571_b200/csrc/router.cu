@@ -628,6 +628,93 @@ __global__ void varlen_count_kernel(const int32_t* __restrict__ topk, int64_t N,
     for (int b = threadIdx.x; b < n_blocks; b += blockDim.x) out[b] = hist[b];
 }
 
+// Column scan split 4 ways: a CTA takes 32 block columns, its 4 warps each
+// a quarter of the chunks (first pass: segment sums; second pass: rescan the
+// segment from its base, the reads hit L2). The one-CTA-per-head scan had
+// each thread walk all chunks of a column in dependent batches of 16 loads.
+__global__ void __launch_bounds__(128)
+varlen_scan_cols_kernel(int32_t* __restrict__ cc, int n_blocks, int n_chunks, int32_t* __restrict__ counts) {
+    __shared__ int32_t part[4][32];
+    const int64_t h = blockIdx.y;
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const int b = blockIdx.x * 32 + lane;
+    const int L = (n_chunks + 3) / 4;
+    const int c_lo = min(n_chunks, seg * L), c_hi = min(n_chunks, (seg + 1) * L);
+    int32_t* col = cc + h * (int64_t)n_chunks * n_blocks + b;
+    int32_t sum = 0;
+    if (b < n_blocks) {
+        int c = c_lo;
+        for (; c + 16 <= c_hi; c += 16) {
+            int32_t v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = col[(int64_t)(c + u) * n_blocks];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) sum += v[u];
+        }
+        for (; c < c_hi; ++c) sum += col[(int64_t)c * n_blocks];
+    }
+    part[seg][lane] = sum;
+    __syncthreads();
+    if (b >= n_blocks) return;
+    int32_t run = 0;
+    for (int s2 = 0; s2 < seg; ++s2) run += part[s2][lane];
+    if (seg == 3) counts[h * n_blocks + b] = run + sum;
+    int c = c_lo;
+    for (; c + 16 <= c_hi; c += 16) {
+        int32_t v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = col[(int64_t)(c + u) * n_blocks];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            col[(int64_t)(c + u) * n_blocks] = run;
+            run += v[u];
+        }
+    }
+    for (; c < c_hi; ++c) {
+        const int32_t v = col[(int64_t)c * n_blocks];
+        col[(int64_t)c * n_blocks] = run;
+        run += v;
+    }
+}
+
+// per head: offsets = exclusive scan of the block counts, 1024 at a time
+__global__ void __launch_bounds__(1024)
+varlen_offsets_kernel(const int32_t* __restrict__ counts, int n_blocks, int32_t* __restrict__ offsets) {
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t carry;
+    const int64_t h = blockIdx.x;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < n_blocks; b0 += 1024) {
+        int b = b0 + threadIdx.x;
+        int32_t v = (b < n_blocks) ? counts[h * n_blocks + b] : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int32_t t = warp_tot[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_tot[lane] = t;  // inclusive
+        }
+        __syncthreads();
+        int32_t excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - v;
+        if (b < n_blocks) offsets[h * n_blocks + b] = excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += warp_tot[31];
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(1024)
 varlen_scan_kernel(int32_t* __restrict__ cc, int n_blocks, int n_chunks, int32_t* __restrict__ counts,
                    int32_t* __restrict__ offsets) {
@@ -928,8 +1015,15 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
         cudaStreamSynchronize(s);
         if (herr) return MOBA_ERR_PLAN;
     }
-    varlen_scan_kernel<<<(unsigned)bh, 1024, 0, s>>>(cc, g.n_blocks, g.n_chunks, counts, offsets);
-    st = check_launch("varlen_scan_kernel");
+    if (g.n_chunks >= 64) {
+        varlen_scan_cols_kernel<<<dim3((unsigned)ceil_div(g.n_blocks, 32), (unsigned)bh), 128, 0, s>>>(
+            cc, g.n_blocks, g.n_chunks, counts);
+        varlen_offsets_kernel<<<(unsigned)bh, 1024, 0, s>>>(counts, g.n_blocks, offsets);
+        st = check_launch("varlen_scan_cols_kernel", 2);
+    } else {
+        varlen_scan_kernel<<<(unsigned)bh, 1024, 0, s>>>(cc, g.n_blocks, g.n_chunks, counts, offsets);
+        st = check_launch("varlen_scan_kernel");
+    }
     if (st) return st;
     const size_t rsmem = (size_t)g.TQ * width * sizeof(int32_t);
     const size_t ssmem4 = 4 * hsmem + rsmem;
