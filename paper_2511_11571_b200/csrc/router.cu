@@ -615,12 +615,23 @@ __global__ void varlen_count_kernel(const int32_t* __restrict__ topk, int64_t N,
     const int64_t i0 = (int64_t)chunk * TQ;
     const int64_t i1 = min64(i0 + TQ, N);
     const int32_t* base = topk + h * N * width;
-    for (int64_t e = i0 * width + threadIdx.x; e < i1 * width; e += blockDim.x) {
-        int b = base[e];
-        if (b >= n_blocks || b < -1) {
-            atomicOr(err, 1);
-        } else if (b >= 0) {
-            atomicAdd(&hist[b], 1);
+    // 8 loads in flight per thread before the shared-memory atomics
+    const int64_t e_end = i1 * width;
+    for (int64_t e0 = i0 * width + threadIdx.x; e0 < e_end; e0 += 8 * (int64_t)blockDim.x) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t e = e0 + (int64_t)u * blockDim.x;
+            v[u] = (e < e_end) ? __ldg(base + e) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int b = v[u];
+            if (b >= n_blocks || b < -1) {
+                atomicOr(err, 1);
+            } else if (b >= 0) {
+                atomicAdd(&hist[b], 1);
+            }
         }
     }
     __syncthreads();
