@@ -77,13 +77,22 @@ struct Item {
     int64_t kb0, fl_base;   // first key row (head-local), head-local flat base of the slice
 };
 
-MOBA_DEV Item decode(int it, int64_t bh, int n_blocks, int slabs, int B, int64_t N, int width,
+// Items run in groups of `hg` heads (the group's fp32 dQ rows fit in L2, so
+// the dQ reductions stay on chip when N is large), block-major inside a
+// group: block 0 of every head of the group first (early blocks are selected
+// by the most queries, so this is close to longest-first).
+MOBA_DEV Item decode(int it, int64_t bh, int hg, int n_blocks, int slabs, int B, int64_t N, int width,
                      const int32_t* counts, const int32_t* offsets) {
     Item x;
-    const int per_j = (int)(bh * slabs);
-    x.j = it / per_j;
-    const int rem = it % per_j;
-    x.h = rem / slabs;
+    const int per_group = hg * n_blocks * slabs;
+    const int g = it / per_group;
+    const int r = it - g * per_group;
+    const int h0 = g * hg;
+    const int hn = (int)min64(hg, bh - h0);
+    const int per_j = hn * slabs;
+    x.j = r / per_j;
+    const int rem = r % per_j;
+    x.h = h0 + rem / slabs;
     x.slab = rem % slabs;
     const int64_t hj = x.h * n_blocks + x.j;
     x.cnt = counts[hj];
@@ -111,7 +120,7 @@ struct RingReader {
 __global__ void __launch_bounds__(kThreads, 1)
 moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ dO,
                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                     const float* __restrict__ lse, const float* __restrict__ Dd, int64_t bh, int kv_group, int64_t N,
+                     const float* __restrict__ lse, const float* __restrict__ Dd, int64_t bh, int hg, int kv_group, int64_t N,
                      int B, int width, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                      const int32_t* __restrict__ flat, float scale, int n_items, int* __restrict__ sched,
                      float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
@@ -188,7 +197,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 it = rr.next(bars, lane);
             }
             if (it < 0) break;
-            const Item x = decode(it, bh, n_blocks, slabs, B, N, width, counts, offsets);
+            const Item x = decode(it, bh, hg, n_blocks, slabs, B, N, width, counts, offsets);
             if (x.n_tiles == 0) continue;
             if (warp == 0) {
                 const int ks = kv_use & 1;
@@ -267,7 +276,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
             while (t_in == n_in) {
                 const int it = rr.next(bars, lane);
                 if (it < 0) return false;
-                const Item x = decode(it, bh, n_blocks, slabs, B, N, width, counts, offsets);
+                const Item x = decode(it, bh, hg, n_blocks, slabs, B, N, width, counts, offsets);
                 if (x.n_tiles == 0) continue;
                 n_in = x.n_tiles;
                 t_in = 0;
@@ -364,7 +373,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
         for (;;) {
             const int it = rr.next(bars, lane);
             if (it < 0) break;
-            const Item x = decode(it, bh, n_blocks, slabs, B, N, width, counts, offsets);
+            const Item x = decode(it, bh, hg, n_blocks, slabs, B, N, width, counts, offsets);
             const int64_t key = x.kb0 + row;
             const bool krow_ok = row < x.klen;
             for (int t = 0; t < x.n_tiles; ++t, ++g) {
@@ -472,7 +481,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
         for (;;) {
             const int it = rr.next(bars, lane);
             if (it < 0) break;
-            const Item x = decode(it, bh, n_blocks, slabs, B, N, width, counts, offsets);
+            const Item x = decode(it, bh, hg, n_blocks, slabs, B, N, width, counts, offsets);
             for (int t = 0; t < x.n_tiles; ++t, ++g) {
                 const int st = g % kQSt;
                 mbar_wait(&bars->dq_full[g & 1], (g >> 1) & 1);
@@ -579,6 +588,10 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
         return MOBA_ERR_CUDA;
     const int64_t n_items = bh * ceil_div(N, B) * ceil_div(B, KT);
     if (n_items >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
+    // heads per item group: the group's fp32 dQ accumulator rows <= 48 MB
+    static const int hg_env = std::getenv("MOBA_BWD_HEAD_GROUP") ? std::atoi(std::getenv("MOBA_BWD_HEAD_GROUP")) : 0;
+    const int hg = (int)std::min<int64_t>(bh, hg_env > 0 ? hg_env
+                                                        : std::max<int64_t>(1, (48ll << 20) / (N * D * 4)));
     cudaMemsetAsync(sched, 0, sizeof(int), s);
     auto kern = moba_bwd_pipe_kernel;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
@@ -587,7 +600,7 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
     const char* trace_path = std::getenv("MOBA_BWD_TRACE");
     if (trace_path != nullptr && trace == nullptr) cudaMalloc(&trace, 256 * 16 * sizeof(long long));
     if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
-    kern<<<grid, kThreads, kSmem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, bh,
+    kern<<<grid, kThreads, kSmem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, bh, hg,
                                        kv_group, N, B, width, counts, offsets, flat, scale, (int)n_items, sched, dq_acc, dq_part,
                                        part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
                                        trace_path != nullptr ? trace : nullptr);
