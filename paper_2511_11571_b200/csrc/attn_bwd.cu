@@ -292,10 +292,13 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     uint8_t* k_s = smem;
     uint8_t* v_s = k_s + kv_bytes;
     uint8_t* dst_s = v_s + kv_bytes;                 // dS^T  [2 q-slabs][128 keys][128B] (A of dQ)
-    uint8_t* stg_s = dst_s + pt_bytes;               // dQ staging: 128 rows x (D fp32 + 16 B pad)
-    constexpr bool kStage = (D == 64);               // D = 128 has no room for it
+    uint8_t* stg_s = dst_s + pt_bytes;               // dQ staging: kStgRows rows x (D fp32 + 16 B pad)
+    constexpr bool kStage = true;
+    // D = 128: 64 staged rows (each epilogue warp stages its 32 rows in two
+    // rounds of 16), which fits beside the single Q/dO stage
+    constexpr int kStgRows = (D == 64) ? 128 : 64;
     constexpr uint32_t kStgRow = D * 4 + 16;
-    uint8_t* stage0 = stg_s + (kStage ? (MQ * kStgRow + 1023) / 1024 * 1024 : 0);   // per stage: Q | dO | L | D | qid
+    uint8_t* stage0 = stg_s + (kStage ? (kStgRows * kStgRow + 1023) / 1024 * 1024 : 0);   // per stage: Q | dO | L | D | qid
     constexpr uint32_t stage_bytes = (2 * qt_bytes + 3 * MQ * 4 + 1023) / 1024 * 1024;  // SW128 tiles need 1 KB alignment
     BwdBars* bars = reinterpret_cast<BwdBars*>(stage0 + qstages * stage_bytes);
 
@@ -636,6 +639,39 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                             }
                         }
                     }
+                } else if constexpr (D == 128) {
+                    // two rounds of 16 lanes over 16 staged rows per warp; every
+                    // lane takes part in the (warp-collective) TMEM loads
+                    const uint32_t srow = smem_u32(stg_s) + (quad * 16 + (lane & 15)) * kStgRow;
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        bulk_wait_read0();               // this lane's previous bulk op has read its row
+                        __syncwarp();
+                        const bool mine = (lane >> 4) == rr;
+#pragma unroll
+                        for (int c0 = 0; c0 < D; c0 += 32) {
+                            float v[32];
+                            tmem_ld32(t_dq + lane_off + c0, v);
+                            tmem_ld_wait();
+                            if (mine) {
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4)
+                                    sts128(srow + (c0 + i) * 4,
+                                           make_uint4(__float_as_uint(v[i]), __float_as_uint(v[i + 1]),
+                                                      __float_as_uint(v[i + 2]), __float_as_uint(v[i + 3])));
+                            }
+                        }
+                        if (mine) {
+                            fence_proxy_async_smem();
+                            if (qi >= 0) {
+                                if (dq_part != nullptr)
+                                    bulk_store(dq_part + slab * part_stride + (pbase + r_in) * D, srow, D * 4);
+                                else
+                                    bulk_reduce_add_f32(dq_acc + (h * N + qi) * D, srow, D * 4);
+                            }
+                            bulk_commit();
+                        }
+                    }
                 } else {
                 // TMEM -> padded fp32 staging row -> one bulk reduce (or store) per row
                 const uint32_t srow = smem_u32(stg_s) + row * kStgRow;
@@ -847,7 +883,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                                         dq_acc, dq_part, part_stride, dk, dv, s);
     } else {
         const size_t stage_bytes = align_up(2 * (size_t)128 * D * 2 + 3 * 128 * 4, 1024);
-        const size_t stg_bytes = (D == 64) ? align_up((size_t)128 * (D * 4 + 16), 1024) : 0;
+        const size_t stg_bytes = align_up((size_t)(D == 64 ? 128 : 64) * (D * 4 + 16), 1024);
         const size_t fixed = 1024 + 2 * (size_t)128 * D * 2 + (size_t)128 * 128 * 2 + stg_bytes + sizeof(BwdBars);
         const int qstages = (fixed + 2 * stage_bytes <= 232448) ? 2 : 1;
         const size_t smem = fixed + qstages * stage_bytes;
