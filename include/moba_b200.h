@@ -77,6 +77,16 @@ int moba_centroids(const void* k, const float* conv_w, int conv_width,
                    int64_t bh, int64_t n_tokens, int head_dim, int block_size,
                    void* k_conv_out, float* centroids, void* stream);
 
+/*
+ * moba_centroids with fp32 keys (numpy f32 / f64 callers of
+ * compute_centroids / key_conv_forward, src/router.py:32-46): the centroids
+ * (and the conv's unrounded K') come from the caller's unrounded keys;
+ * k_conv_out is still bf16 (the attention operand).
+ */
+int moba_centroids_f32(const float* k, const float* conv_w, int conv_width,
+                       int64_t bh, int64_t n_tokens, int head_dim, int block_size,
+                       void* k_conv_out, float* centroids, void* stream);
+
 /* Workspace bytes needed by moba_route / moba_varlen. */
 size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int block_size, int top_k);
 
@@ -95,6 +105,17 @@ int moba_route(const void* q, const float* centroids,
                int32_t* topk, int32_t* counts, int32_t* offsets,
                int32_t* flat, int32_t* row_pos,
                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * moba_route_gqa in fp32 routing mode with fp32 queries [bh, n_tokens,
+ * head_dim] (numpy f32 / f64 callers of select_topk, src/router.py:49-120):
+ * scores are exact fp32 products of the caller's unrounded q and the fp32
+ * centroids, so routing is not perturbed by rounding Q to bf16.
+ */
+int moba_route_f32(const float* q, const float* centroids, int64_t bh, int kv_group,
+                   int64_t n_tokens, int head_dim, int block_size, int top_k,
+                   int32_t* topk, int32_t* counts, int32_t* offsets, int32_t* flat, int32_t* row_pos,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Stage 3 alone — varlen layout from a caller-supplied index matrix
@@ -220,6 +241,7 @@ int moba_conv_bwd(const void* k, const float* conv_w, int conv_width, const void
  */
 unsigned long long moba_launch_count(void);
 void moba_timing_enable(int on);
+int moba_timing_enabled(void);
 void moba_timing_reset(void);
 int moba_timing_read(const char* stage, double* total_ms, long long* launches);
 

@@ -4,8 +4,12 @@ The reference's operators take 2-D numpy arrays [N, d] per head
 (src/reference.py:29-33). The drop-in accepts those (results come back as
 numpy in the input's float dtype) and, for the fast path, torch tensors of
 shape [N, d], [H, N, d] or [b, H, N, d] (results stay on the GPU in bf16 /
-fp32). Internally everything is bf16 [H, N, Dp] with Dp in {64, 128}; the
-extra channels are zero, which leaves every dot product unchanged.
+fp32). Internally the attention operands are bf16 [H, N, Dp] with Dp in
+{64, 128}; the extra channels are zero, which leaves every dot product
+unchanged. Callers whose Q / K are not bf16 (numpy f32 / f64, torch fp32 /
+fp64 / fp16) also get an fp32 copy: centroids and routing are computed from
+the unrounded values (to_heads_f32), so the block selection is not moved by
+the bf16 rounding of the attention operands.
 """
 
 from __future__ import annotations
@@ -36,8 +40,8 @@ def _device_for(x):
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def to_heads(x, name: str = "tensor", device=None):
-    """-> (bf16 CUDA tensor [H, N, Dp], HeadsInfo)."""
+def to_heads(x, name: str = "tensor", device=None, dtype=torch.bfloat16):
+    """-> (CUDA tensor [H, N, Dp] of `dtype` (bf16 by default), HeadsInfo)."""
     if isinstance(x, np.ndarray) or not isinstance(x, torch.Tensor):
         arr = np.asarray(x)
         if arr.ndim < 2:
@@ -55,10 +59,23 @@ def to_heads(x, name: str = "tensor", device=None):
         dev = device or _device_for(x)
         t = x.to(dev)
     info.device = dev
-    t = t.to(torch.bfloat16).reshape(-1, info.n_tokens, info.d)
+    t = t.to(dtype).reshape(-1, info.n_tokens, info.d)
     if info.dp != info.d:
         t = torch.nn.functional.pad(t, (0, info.dp - info.d))
     return t.contiguous(), info
+
+
+def needs_fp32_routing(x) -> bool:
+    """True unless x is already bf16 (then rounding it changes nothing)."""
+    return not (isinstance(x, torch.Tensor) and x.dtype == torch.bfloat16)
+
+
+def routing_heads(x, name: str, device=None):
+    """fp32 [H, N, Dp] copy for centroids / routing when x is not bf16, else None."""
+    if not needs_fp32_routing(x):
+        return None
+    t, _ = to_heads(x, name, device=device, dtype=torch.float32)
+    return t
 
 
 def from_heads(t: torch.Tensor, info: HeadsInfo, channels: bool = True):

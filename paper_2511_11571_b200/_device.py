@@ -42,7 +42,9 @@ def _stream(t: torch.Tensor) -> int:
 
 def centroids(k: torch.Tensor, block_size: int, conv_w: torch.Tensor | None = None):
     """(centroids fp32 [H, n, Dp], k_used bf16 [H, N, Dp]); k_used is the
-    conv output when conv_w is given, else k itself."""
+    conv output when conv_w is given, else k itself. An fp32 `k` (numpy f32 /
+    f64 callers) is pooled unrounded; its k_used is the bf16 copy (or the
+    bf16 K' of the conv)."""
     lib = _lib.load()
     H, N, Dp = k.shape
     n = -(-N // block_size)
@@ -52,11 +54,13 @@ def centroids(k: torch.Tensor, block_size: int, conv_w: torch.Tensor | None = No
     if conv_w is not None:
         width = int(conv_w.shape[0])
         conv_w = conv_w.to(device=k.device, dtype=torch.float32).contiguous()
-        k_out = torch.empty_like(k)
-    st = lib.moba_centroids(k.data_ptr(), _lib.ptr(conv_w), width, H, N, Dp, block_size,
-                            _lib.ptr(k_out), cent.data_ptr(), _stream(k))
+        k_out = torch.empty((H, N, Dp), dtype=torch.bfloat16, device=k.device)
+    fn = lib.moba_centroids_f32 if k.dtype == torch.float32 else lib.moba_centroids
+    st = fn(k.data_ptr(), _lib.ptr(conv_w), width, H, N, Dp, block_size, _lib.ptr(k_out), cent.data_ptr(), _stream(k))
     _lib.check(st, "moba_centroids")
-    return cent, (k_out if k_out is not None else k)
+    if k_out is not None:
+        return cent, k_out
+    return cent, (k.to(torch.bfloat16) if k.dtype != torch.bfloat16 else k)
 
 
 def _empty_plan(H, N, width, n, device):
@@ -85,10 +89,17 @@ def route(q: torch.Tensor, cent: torch.Tensor, block_size: int, top_k: int, mode
     width = top_k + 1
     topk, counts, offsets, flat, row_pos = _empty_plan(H, N, width, n, q.device)
     ws = _ws(lib.moba_route_workspace_size(H, N, block_size, top_k), q.device)
-    st = lib.moba_route_gqa(q.data_ptr(), cent.data_ptr(), H, G, N, Dp, block_size, top_k, mode,
-                        topk.data_ptr(), counts.data_ptr(), offsets.data_ptr(), flat.data_ptr(),
-                        row_pos.data_ptr(), ws.data_ptr(), ws.numel(), _stream(q))
-    _lib.check(st, "moba_route_gqa")
+    if q.dtype == torch.float32 and mode == _lib.MOBA_ROUTE_FP32:
+        # numpy f32 / f64 callers: route on the unrounded queries
+        st = lib.moba_route_f32(q.data_ptr(), cent.data_ptr(), H, G, N, Dp, block_size, top_k,
+                                topk.data_ptr(), counts.data_ptr(), offsets.data_ptr(), flat.data_ptr(),
+                                row_pos.data_ptr(), ws.data_ptr(), ws.numel(), _stream(q))
+    else:
+        qb = q if q.dtype == torch.bfloat16 else q.to(torch.bfloat16)
+        st = lib.moba_route_gqa(qb.data_ptr(), cent.data_ptr(), H, G, N, Dp, block_size, top_k, mode,
+                                topk.data_ptr(), counts.data_ptr(), offsets.data_ptr(), flat.data_ptr(),
+                                row_pos.data_ptr(), ws.data_ptr(), ws.numel(), _stream(q))
+    _lib.check(st, "moba_route")
     return RoutingPlan(topk, counts, offsets, flat, row_pos, N, block_size)
 
 

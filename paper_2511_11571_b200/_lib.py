@@ -38,6 +38,7 @@ SIGNATURES = {
     "moba_status_string": (ctypes.c_char_p, [_i32]),
     "moba_last_error": (ctypes.c_char_p, []),
     "moba_centroids": (_i32, [_p, _p, _i32, _i64, _i64, _i32, _i32, _p, _p, _p]),
+    "moba_centroids_f32": (_i32, [_p, _p, _i32, _i64, _i64, _i32, _i32, _p, _p, _p]),
     "moba_route_workspace_size": (_sz, [_i64, _i64, _i32, _i32]),
     "moba_route": (_i32, [_p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "moba_varlen": (_i32, [_p, _i64, _i64, _i32, _i32, _p, _p, _p, _p, _p, _sz, _p]),
@@ -49,6 +50,7 @@ SIGNATURES = {
     "moba_bwd": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _i32,
                         _f32, _p, _p, _p, _p, _sz, _p]),
     "moba_route_gqa": (_i32, [_p, _p, _i64, _i32, _i64, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "moba_route_f32": (_i32, [_p, _p, _i64, _i32, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "moba_fwd_gqa": (_i32, [_p, _p, _p, _i64, _i32, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _f32, _p, _p, _p, _sz,
                             _p]),
     "moba_bwd_gqa_workspace_size": (_sz, [_i64, _i32, _i64, _i32, _i32, _i32, _i32]),
@@ -58,6 +60,7 @@ SIGNATURES = {
     "moba_conv_bwd": (_i32, [_p, _p, _i32, _p, _i64, _i64, _i32, _p, _p, _p, _sz, _p]),
     "moba_launch_count": (ctypes.c_ulonglong, []),
     "moba_timing_enable": (None, [_i32]),
+    "moba_timing_enabled": (_i32, []),
     "moba_timing_reset": (None, []),
     "moba_timing_read": (_i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_longlong)]),

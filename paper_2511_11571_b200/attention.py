@@ -8,9 +8,11 @@ Reference-shaped entry points (same names, argument meaning, errors):
 plus the torch-facing, autograd-enabled batched call used by training code:
   moba_attn(q, k, v, block_size, top_k, causal=True, conv_weight=None)
 
-Numerics: the kernels compute in bf16 with fp32 accumulation and fp32 LSE;
-f32/f64 numpy inputs are rounded to bf16 on upload (the tolerance contract
-is max-abs 2e-2 / rel-L2 1e-2 against the reference on the same inputs).
+Numerics: the attention kernels compute in bf16 with fp32 accumulation and
+fp32 LSE; f32/f64 inputs are rounded to bf16 for the attention operands
+(the tolerance contract is max-abs 2e-2 / rel-L2 1e-2 against the reference
+on the same inputs), while centroids and fp32-mode routing use the unrounded
+values, so block selection matches the reference up to score ties.
 """
 
 from __future__ import annotations
@@ -21,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _device
-from ._convert import from_heads, to_heads, to_weights
+from ._convert import from_heads, routing_heads, to_heads, to_weights
 from .core import (ConfigError, MobaConfig, OpCounters, PlanValidationError, RoutingPlan, ShapeError,
                    resolve_threads)
 from .router import ROUTE_MODES, build_plan
@@ -118,14 +120,17 @@ def moba_attention(Q, K, V, cfg: MobaConfig, counters: OpCounters | None = None,
     q, info = to_heads(Q, "Q")
     k, _ = to_heads(K, "K", device=q.device)
     v, _ = to_heads(V, "V", device=q.device)
+    k32 = routing_heads(K, "K", device=q.device)       # unrounded keys for the centroids (non-bf16 callers)
+    k_src = k if k32 is None else k32
     if kernel is not None:
         w = to_weights(getattr(kernel, "weights", kernel), info.d, info.dp, q.device)
-        cent, k = _device.centroids(k, cfg.block_size_B, w)
+        cent, k = _device.centroids(k_src, cfg.block_size_B, w)
     else:
-        cent, _ = _device.centroids(k, cfg.block_size_B)
+        cent, _ = _device.centroids(k_src, cfg.block_size_B)
     if cfg.top_k > _device.MAX_TOP_K:
         raise ConfigError(f"top_k={cfg.top_k} is not supported by the compiled kernels")
-    plan = _device.route(q, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])
+    q32 = routing_heads(Q, "Q", device=q.device) if mode == "fp32" else None
+    plan = _device.route(q if q32 is None else q32, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])
     out, lse = _device.fwd(q, k, v, plan, _device.softmax_scale(info.d))
     if counters is not None:
         H = q.shape[0]

@@ -231,8 +231,10 @@ class RoutingPlan:
     def head(self, h: int) -> "RoutingPlan":
         """Single-head view (device tensors are sliced, not copied)."""
         sl = slice(h, h + 1)
-        return RoutingPlan(self.topk[sl], self.counts_d[sl], self.offsets_d[sl], self.flat_d[sl],
-                           None if self.row_pos is None else self.row_pos[sl],
+        # a stale inverse map (a field was reassigned) is not handed down:
+        # the child rebuilds it from its own fields when it needs it
+        rp = None if (self.row_pos is None or self._row_pos_stale) else self.row_pos[sl]
+        return RoutingPlan(self.topk[sl], self.counts_d[sl], self.offsets_d[sl], self.flat_d[sl], rp,
                            self.n_tokens, self.block_size)
 
 

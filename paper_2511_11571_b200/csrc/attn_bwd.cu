@@ -2,245 +2,23 @@
 // src/attention.py:239-302; paper Alg. 5).
 //
 //   bwd_preprocess : D = rowsum(dO * O) (src/attention.py:266), zero dQ_acc
-//   bwd main       : one CTA per (head, key block, <=128-key slab). K_j/V_j
-//                    stay in shared memory; the CTA walks the block's varlen
-//                    slice in 64-query tiles, gathers Q/dO/L/D, recomputes
-//                    S and P = exp(S - L) (src/attention.py:229), and
-//                    accumulates dV_j += P^T dO, dK_j += dS^T Q in registers
+//   bwd main       : per (head, key block, <=128-key slab) item, K_j/V_j
+//                    stay on chip; the item's varlen slice is walked in
+//                    128-query tiles: gather Q/dO/L/D, recompute S and
+//                    P = exp(S - L) (src/attention.py:229), accumulate
+//                    dV_j += P^T dO, dK_j += dS^T Q in TMEM
 //                    (src/attention.py:230-233); dQ += dS K_j goes to an
-//                    fp32 accumulator with vector reductions
-//                    (src/attention.py:234).
+//                    fp32 accumulator with bulk reductions
+//                    (src/attention.py:234). d = 64: attn_bwd_pipe.cu;
+//                    d = 128: moba_bwd_tc_kernel below.
 //   bwd_finalize   : dQ = dQ_acc * scale -> bf16 (src/attention.py:299)
-//
-// This is the legacy-MMA (mma.sync m16n8k16) path.
 #include "common.cuh"
-#include <type_traits>
 #include "sm100.cuh"
 #include <cstdlib>
 
 namespace moba {
 
-constexpr int kBwdBM = 64;  // gathered queries per tile
 constexpr float kLog2eB = 1.4426950408889634f;
-
-template <int D, int KT>
-__global__ void __launch_bounds__(KT * 2)
-moba_bwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K,
-                    const __nv_bfloat16* __restrict__ V, const __nv_bfloat16* __restrict__ dO,
-                    const float* __restrict__ lse, const float* __restrict__ Dd, int64_t N, int B, int width,
-                    const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
-                    const int32_t* __restrict__ flat, float scale, float* __restrict__ dq_acc,
-                    float* __restrict__ dq_part, int64_t part_stride,
-                    __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV) {
-    constexpr int RB = D * 2;
-    constexpr int CH = D / 8;
-    constexpr int NW = KT / 16;          // warps: 16 keys each
-    constexpr int NT = NW * 32;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* k_s = smem;
-    uint8_t* v_s = k_s + KT * RB;
-    uint8_t* q_s = v_s + KT * RB;
-    uint8_t* do_s = q_s + kBwdBM * RB;
-    uint8_t* ds_s = do_s + kBwdBM * RB;  // [KT keys][64 queries] bf16, 128 B rows
-    float* l_s = reinterpret_cast<float*>(ds_s + KT * 128);
-    float* d_s = l_s + kBwdBM;
-    int32_t* qid_s = reinterpret_cast<int32_t*>(d_s + kBwdBM);
-
-    const int n_blocks = (int)((N + B - 1) / B);
-    const int slabs = (B + KT - 1) / KT;
-    const int j = blockIdx.x / slabs;
-    const int slab = blockIdx.x % slabs;
-    const int64_t h = blockIdx.y;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int g = lane >> 2, t4 = lane & 3;
-
-    const int64_t kb0 = (int64_t)j * B + slab * KT;           // first key of the slab
-    const int klen = (int)max64(0, min64(min64((int64_t)KT, (int64_t)B - slab * KT), N - kb0));
-    const int hj = (int)(h * n_blocks + j);
-    const int cnt = counts[hj];
-    const int32_t* fl = flat + h * N * width + offsets[hj];
-    const __nv_bfloat16* Qh = Q + h * N * D;
-    const __nv_bfloat16* dOh = dO + h * N * D;
-
-    for (int e = tid; e < KT * CH; e += NT) {
-        int r = e / CH, c = e % CH;
-        bool ok = r < klen;
-        int64_t src = (h * N + kb0 + (ok ? r : 0)) * D + c * 8;
-        cp_async16(smem_u32(k_s + swz<RB>(r, c)), K + src, ok);
-        cp_async16(smem_u32(v_s + swz<RB>(r, c)), V + src, ok);
-    }
-    cp_async_commit();
-
-    const int m0 = warp * 16;  // this warp's keys within the slab
-    float dk[D / 8][4], dv[D / 8][4];
-#pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) dk[nt][e] = dv[nt][e] = 0.f;
-
-    const float sl2 = scale * kLog2eB;
-    for (int r0 = 0; r0 < cnt; r0 += kBwdBM) {
-        const int rows = min(kBwdBM, cnt - r0);
-        __syncthreads();  // previous tile fully consumed
-        if (tid < kBwdBM) {
-            int qi = (tid < rows) ? fl[r0 + tid] : -1;
-            qid_s[tid] = qi;
-            l_s[tid] = (qi >= 0) ? lse[h * N + qi] * kLog2eB : 0.f;
-            d_s[tid] = (qi >= 0) ? Dd[h * N + qi] : 0.f;
-        }
-        __syncthreads();
-        for (int e = tid; e < kBwdBM * CH; e += NT) {
-            int r = e / CH, c = e % CH;
-            int qi = qid_s[r];
-            int64_t src = (int64_t)max(qi, 0) * D + c * 8;
-            cp_async16(smem_u32(q_s + swz<RB>(r, c)), Qh + src, qi >= 0);
-            cp_async16(smem_u32(do_s + swz<RB>(r, c)), dOh + src, qi >= 0);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-
-        // ---- S^T = K_w Q^T  (16 keys x 64 queries) and dP^T = V_w dO^T
-        float s[8][4], dp[8][4];
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) s[nt][e] = dp[nt][e] = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-            uint32_t ka[4], va[4];
-            {
-                int r = m0 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                int c = kk * 2 + (lane >> 4);
-                ldmatrix_x4(smem_u32(k_s + swz<RB>(r, c)), ka[0], ka[1], ka[2], ka[3]);
-                ldmatrix_x4(smem_u32(v_s + swz<RB>(r, c)), va[0], va[1], va[2], va[3]);
-            }
-#pragma unroll
-            for (int np = 0; np < 4; ++np) {
-                int r = np * 16 + (lane & 7) + (lane >> 4) * 8;
-                int c = kk * 2 + ((lane >> 3) & 1);
-                uint32_t b0, b1, b2, b3;
-                ldmatrix_x4(smem_u32(q_s + swz<RB>(r, c)), b0, b1, b2, b3);
-                mma_bf16_16816(s[2 * np], ka, b0, b1);
-                mma_bf16_16816(s[2 * np + 1], ka, b2, b3);
-                ldmatrix_x4(smem_u32(do_s + swz<RB>(r, c)), b0, b1, b2, b3);
-                mma_bf16_16816(dp[2 * np], va, b0, b1);
-                mma_bf16_16816(dp[2 * np + 1], va, b2, b3);
-            }
-        }
-        // ---- P^T, dS^T (element: key row m0+g(+8), query col nt*8+2t4(+1))
-        const int key_lo = m0 + g, key_hi = m0 + g + 8;
-        uint32_t pa[4][4], dsa[4][4];
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-            float pv[4], dsv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                int qc = nt * 8 + 2 * t4 + (e & 1);
-                int key = (e < 2) ? key_lo : key_hi;
-                int qi = qid_s[qc];
-                bool ok = qi >= 0 && key < klen && (kb0 + key) <= (int64_t)qi;
-                float p = ok ? fast_exp2(s[nt][e] * sl2 - l_s[qc]) : 0.f;
-                pv[e] = p;
-                dsv[e] = p * (dp[nt][e] - d_s[qc]);
-            }
-            pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(pv[0], pv[1]);
-            pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(pv[2], pv[3]);
-            dsa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(dsv[0], dsv[1]);
-            dsa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(dsv[2], dsv[3]);
-            // dS^T to smem for the dQ product: row = key, col = query
-            *reinterpret_cast<uint32_t*>(ds_s + swz<128>(key_lo, nt) + 4 * t4) = dsa[nt >> 1][(nt & 1) * 2 + 0];
-            *reinterpret_cast<uint32_t*>(ds_s + swz<128>(key_hi, nt) + 4 * t4) = dsa[nt >> 1][(nt & 1) * 2 + 1];
-        }
-        // ---- dV += P^T dO ; dK += dS^T Q   (k = query)
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-#pragma unroll
-            for (int np = 0; np < D / 16; ++np) {
-                int r = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                int c = np * 2 + (lane >> 4);
-                uint32_t b0, b1, b2, b3;
-                ldmatrix_x4_trans(smem_u32(do_s + swz<RB>(r, c)), b0, b1, b2, b3);
-                mma_bf16_16816(dv[2 * np], pa[ks], b0, b1);
-                mma_bf16_16816(dv[2 * np + 1], pa[ks], b2, b3);
-                ldmatrix_x4_trans(smem_u32(q_s + swz<RB>(r, c)), b0, b1, b2, b3);
-                mma_bf16_16816(dk[2 * np], dsa[ks], b0, b1);
-                mma_bf16_16816(dk[2 * np + 1], dsa[ks], b2, b3);
-            }
-        }
-        __syncthreads();  // ds_s complete
-        // ---- dQ (64 q x D) += dS (64 q x KT keys) K_slab (KT x D)
-        {
-            constexpr int QW = 4;                    // 16-query row groups
-            constexpr int DSPLIT = NW / QW;          // d splits across warps
-            constexpr int DW = D / DSPLIT;           // d columns per warp
-            const int qr = (warp % QW) * 16;
-            const int dc0 = (warp / QW) * DW;
-            float acc[DW / 8][4];
-#pragma unroll
-            for (int nt = 0; nt < DW / 8; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-#pragma unroll
-            for (int kk = 0; kk < KT / 16; ++kk) {
-                uint32_t a[4];
-                {
-                    int key = kk * 16 + (lane & 7) + (lane >> 4) * 8;
-                    int qc = (qr >> 3) + ((lane >> 3) & 1);
-                    ldmatrix_x4_trans(smem_u32(ds_s + swz<128>(key, qc)), a[0], a[1], a[2], a[3]);
-                }
-#pragma unroll
-                for (int np = 0; np < DW / 16; ++np) {
-                    int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-                    int c = (dc0 >> 3) + np * 2 + (lane >> 4);
-                    uint32_t b0, b1, b2, b3;
-                    ldmatrix_x4_trans(smem_u32(k_s + swz<RB>(key, c)), b0, b1, b2, b3);
-                    mma_bf16_16816(acc[2 * np], a, b0, b1);
-                    mma_bf16_16816(acc[2 * np + 1], a, b2, b3);
-                }
-            }
-            const int q_lo = qid_s[qr + g], q_hi = qid_s[qr + g + 8];
-            if (dq_part != nullptr) {
-                // deterministic schedule: one partial per (query, block,
-                // slab) at its flat position, summed in slot order later
-                float* dst = dq_part + slab * part_stride +
-                             (h * N * width + offsets[hj] + r0 + qr) * (int64_t)D;
-#pragma unroll
-                for (int nt = 0; nt < DW / 8; ++nt) {
-                    int col = dc0 + nt * 8 + 2 * t4;
-                    if (q_lo >= 0)
-                        *reinterpret_cast<float2*>(dst + (int64_t)g * D + col) = make_float2(acc[nt][0], acc[nt][1]);
-                    if (q_hi >= 0)
-                        *reinterpret_cast<float2*>(dst + (int64_t)(g + 8) * D + col) =
-                            make_float2(acc[nt][2], acc[nt][3]);
-                }
-            } else {
-#pragma unroll
-                for (int nt = 0; nt < DW / 8; ++nt) {
-                    int col = dc0 + nt * 8 + 2 * t4;
-                    if (q_lo >= 0) red_add_f32x2(dq_acc + (h * N + q_lo) * D + col, acc[nt][0], acc[nt][1]);
-                    if (q_hi >= 0) red_add_f32x2(dq_acc + (h * N + q_hi) * D + col, acc[nt][2], acc[nt][3]);
-                }
-            }
-        }
-    }
-    cp_async_wait<0>();  // (no-op when the slice was non-empty)
-    // ---- write dK_j = scale * dK, dV_j
-    const int key_lo = m0 + g, key_hi = m0 + g + 8;
-#pragma unroll
-    for (int nt = 0; nt < D / 8; ++nt) {
-        int col = nt * 8 + 2 * t4;
-        if (key_lo < klen) {
-            int64_t o = (h * N + kb0 + key_lo) * D + col;
-            *reinterpret_cast<uint32_t*>(dK + o) = pack_bf16(dk[nt][0] * scale, dk[nt][1] * scale);
-            *reinterpret_cast<uint32_t*>(dV + o) = pack_bf16(dv[nt][0], dv[nt][1]);
-        }
-        if (key_hi < klen) {
-            int64_t o = (h * N + kb0 + key_hi) * D + col;
-            *reinterpret_cast<uint32_t*>(dK + o) = pack_bf16(dk[nt][2] * scale, dk[nt][3] * scale);
-            *reinterpret_cast<uint32_t*>(dV + o) = pack_bf16(dv[nt][2], dv[nt][3]);
-        }
-    }
-}
-
 
 // ---------------------------------------------------------------- tcgen05 path
 // Persistent CTA per (head, key block, 128-key slab) item, 6 warps:
@@ -254,7 +32,6 @@ moba_bwd_mma_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __
 //              per-(query, block) partials); final dK, dV TMEM -> bf16
 // TMEM: S^T [0,128) dP^T [128,256) dV [256,256+D) dK [256+D,256+2D),
 //       dQ [256+2D, 256+3D) when it fits, else aliased onto S^T.
-static long long* g_last_trace = nullptr;
 #define TRACE(slot) do { if (trace && blockIdx.x == 0 && lane == 0 && g < 64) trace[(g) * 16 + (slot)] = clock64(); } while (0)
 
 constexpr int kSmWarps = 8;                               // softmax-bwd warps
@@ -788,10 +565,9 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
 
 // workspace: sched int (256 B) | Dd f32 [bh*N] | dq_acc f32 [bh*N*D] |
 // (deterministic) dq_part f32 [slabs][bh*N*width*D]
-static int bwd_kt(int B) { return B > 64 ? 128 : 64; }
 static size_t bwd_ws(int64_t bh, int64_t N, int D, int B, int width, bool det, int kv_group = 1) {
     size_t w = 256 + align_up((size_t)bh * N * 4, 256) + align_up((size_t)bh * N * D * 4, 256);
-    if (det) w += (size_t)ceil_div(B, bwd_kt(B)) * bh * N * width * D * 4;
+    if (det) w += (size_t)ceil_div(B, 128) * bh * N * width * D * 4;
     if (kv_group > 1) w += 2 * align_up((size_t)bh * N * D * 2, 256);   // per-query-head dK, dV (bf16)
     return w;
 }
@@ -818,23 +594,6 @@ __global__ void gqa_group_sum_kernel(const __nv_bfloat16* __restrict__ src, int6
                                                     pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
 }
 
-template <int D, int KT>
-static int launch_bwd_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
-                           const float* Dd, int64_t bh, int64_t N, int B, int width, const int32_t* counts,
-                           const int32_t* offsets, const int32_t* flat, float scale, float* dq_acc,
-                           float* dq_part, int64_t part_stride, void* dk, void* dv, cudaStream_t s) {
-    const int64_t n = ceil_div(N, B);
-    const int slabs = (int)ceil_div(B, KT);
-    const size_t smem = (size_t)2 * KT * D * 2 + 2 * kBwdBM * D * 2 + KT * 128 + kBwdBM * 12;
-    auto kern = moba_bwd_mma_kernel<D, KT>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((unsigned)(n * slabs), (unsigned)bh);
-    kern<<<grid, KT * 2, smem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
-                                    (const __nv_bfloat16*)dout, lse, Dd, N, B, width, counts, offsets, flat, scale,
-                                    dq_acc, dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
-    return check_launch("moba_bwd_mma_kernel");
-}
-
 template <int D>
 static int launch_bwd(const void* q, const void* k, const void* v, const void* out, const void* dout,
                       const float* lse, int64_t bh, int kv_group, int64_t N, int B, int width, const int32_t* counts,
@@ -846,7 +605,7 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     float* dq_acc = (float*)(ws + align_up((size_t)bh * N * 4, 256));
     float* dq_part = det ? (float*)((uint8_t*)dq_acc + align_up((size_t)bh * N * D * 4, 256)) : nullptr;
     const int64_t part_stride = bh * N * width * D;
-    const int slabs = (int)ceil_div(B, bwd_kt(B));
+    const int slabs = (int)ceil_div(B, 128);
     const int64_t rows = bh * N;
     // GQA: the kernels write per-query-head dK / dV, summed per group below
     void* dk = dk_out;
@@ -866,21 +625,10 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
     if (st) return st;
     {
     StageTimer tm(T_BWD, s);
-    const char* impl = std::getenv("MOBA_BWD_IMPL");
-    const int slabs_tc = (int)ceil_div(B, 128);
-    if (D == 64 && !(impl != nullptr && (impl[0] == 'm' || impl[0] == 't'))) {
+    if (D == 64) {
         // pipelined tcgen05 kernel (attn_bwd_pipe.cu); dq_part slabs follow its 128-key slabs
-        (void)slabs_tc;
         st = launch_bwd_pipe(q, k, v, dout, lse, Dd, bh, kv_group, N, B, width, counts, offsets, flat, scale, sched,
                              dq_acc, dq_part, part_stride, dk, dv, s);
-    } else if (impl != nullptr && impl[0] == 'm') {
-        if (kv_group > 1) return MOBA_ERR_UNSUPPORTED;   // legacy mma.sync kernel: MHA only
-        if (B > 64)
-            st = launch_bwd_main<D, 128>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
-                                         dq_acc, dq_part, part_stride, dk, dv, s);
-        else
-            st = launch_bwd_main<D, 64>(q, k, v, dout, lse, Dd, bh, N, B, width, counts, offsets, flat, scale,
-                                        dq_acc, dq_part, part_stride, dk, dv, s);
     } else {
         const size_t stage_bytes = align_up(2 * (size_t)128 * D * 2 + 3 * 128 * 4, 1024);
         const size_t stg_bytes = align_up((size_t)(D == 64 ? 128 : 64) * (D * 4 + 16), 1024);
@@ -897,7 +645,6 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
             cudaMemsetAsync(tr, 0, 64 * 16 * 8, s);
         }
         long long* trp = tracing ? tr : nullptr;
-        g_last_trace = trp;
         CUtensorMap tm_k, tm_v;
         if (!make_tmap_bf16(&tm_k, k, (uint64_t)(bh / kv_group * N), D, 128) ||
             !make_tmap_bf16(&tm_v, v, (uint64_t)(bh / kv_group * N), D, 128))
@@ -953,6 +700,7 @@ extern "C" int moba_bwd_gqa(const void* q, const void* k, const void* v, const v
                             int width, const int32_t* counts, const int32_t* offsets, const int32_t* flat,
                             const int32_t* row_pos, int deterministic, float softmax_scale, void* dq, void* dk,
                             void* dv, void* workspace, size_t workspace_bytes, void* stream) {
+    clear_last_error();
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
     if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
     if (block_size > 512 || width > 32) return MOBA_ERR_UNSUPPORTED;
@@ -977,10 +725,4 @@ extern "C" int moba_bwd(const void* q, const void* k, const void* v, const void*
                         size_t workspace_bytes, void* stream) {
     return moba_bwd_gqa(q, k, v, out, dout, lse, bh, 1, n_tokens, head_dim, block_size, width, counts, offsets, flat,
                         row_pos, deterministic, softmax_scale, dq, dk, dv, workspace, workspace_bytes, stream);
-}
-
-extern "C" int moba_debug_trace(long long* host, int n) {
-    if (!moba::g_last_trace) return -1;
-    cudaDeviceSynchronize();
-    return (int)cudaMemcpy(host, moba::g_last_trace, n * 8, cudaMemcpyDeviceToHost);
 }

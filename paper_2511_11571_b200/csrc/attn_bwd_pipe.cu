@@ -49,7 +49,6 @@ constexpr uint32_t cS0 = 0, cY = 256, cDV = 384, cDK = 448;
 constexpr uint32_t kStgRow = 64 * 4 + 16;    // full-row dQ staging (fp32) + pad
 constexpr uint32_t kStgRows = 16;            // staged rows per epilogue warp (two rounds of 16 lanes)
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr bool kBwdPolyExp = false;  // MUFU offload for 1 in 4 phase-A exponentials: measured slower (latency bound)
 
 struct Bars {
     uint64_t ring_full[kRing], ring_empty[kRing];
@@ -420,8 +419,7 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                         const float l4[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
-                            sv[i + u] = (kBwdPolyExp && u == 3) ? poly_exp2(fmaf(sv[i + u], sl2, -l4[u]))
-                                                                : fast_exp2(fmaf(sv[i + u], sl2, -l4[u]));
+                            sv[i + u] = fast_exp2(fmaf(sv[i + u], sl2, -l4[u]));
                     }
                 }
                 // sv now holds P (fp32, kept for phase B); bf16 pairs go to TMEM
@@ -589,9 +587,7 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
     const int64_t n_items = bh * ceil_div(N, B) * ceil_div(B, KT);
     if (n_items >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
     // heads per item group: the group's fp32 dQ accumulator rows <= 48 MB
-    static const int hg_env = std::getenv("MOBA_BWD_HEAD_GROUP") ? std::atoi(std::getenv("MOBA_BWD_HEAD_GROUP")) : 0;
-    const int hg = (int)std::min<int64_t>(bh, hg_env > 0 ? hg_env
-                                                        : std::max<int64_t>(1, (48ll << 20) / (N * D * 4)));
+    const int hg = (int)std::min<int64_t>(bh, std::max<int64_t>(1, (48ll << 20) / (N * D * 4)));
     cudaMemsetAsync(sched, 0, sizeof(int), s);
     auto kern = moba_bwd_pipe_kernel;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);

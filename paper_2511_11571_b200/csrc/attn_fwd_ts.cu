@@ -46,7 +46,6 @@ constexpr int kPr0 = 1, kPrN = 3;
 constexpr int kSm0 = 4;       // softmax warps 4-11
 constexpr int kEp0 = 12;      // epilogue warps 12-15
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr bool kPolyExp = false;   // measured slower (issue-bound softmax), kept for experiments
 constexpr uint32_t kStg = 32 * 128;    // per-warp O staging: 32 rows x one 64-column SW128 slab
 
 struct Bars {
@@ -381,7 +380,7 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) ffma2(t[i], t[i + 1], t[i], t[i + 1], scale_log2, scale_log2, -msl, -msl);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) t[i] = (kPolyExp && (i & 3) == 3) ? poly_exp2(t[i]) : fast_exp2(t[i]);
+                    for (int i = 0; i < 32; ++i) t[i] = fast_exp2(t[i]);
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {

@@ -13,6 +13,8 @@ void set_last_error(const char* msg) {
     std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
 }
 
+void clear_last_error() { g_last_error[0] = '\0'; }
+
 static unsigned long long g_launches = 0;
 
 int check_launch(const char* what, int n) {
@@ -183,6 +185,8 @@ extern "C" void moba_timing_enable(int on) {
     moba::drain();
     moba::g_timing = on != 0;
 }
+
+extern "C" int moba_timing_enabled(void) { return moba::g_timing ? 1 : 0; }
 
 extern "C" void moba_timing_reset(void) {
     moba::drain();

@@ -6,6 +6,7 @@
 // when the conv is on, and one fp32 centroid row.
 #include "common.cuh"
 #include <algorithm>
+#include <type_traits>
 
 namespace moba {
 
@@ -99,9 +100,9 @@ centroid_conv_kernel(const __nv_bfloat16* __restrict__ K, const float* __restric
 // rows with all of its loads in flight before any is summed, lane groups
 // are folded with shuffles and the 4 warps through shared memory. The
 // per-column summation order is fixed (deterministic).
-template <int D>
+template <int D, typename KT>
 __global__ void __launch_bounds__(128)
-centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int64_t total_blocks,
+centroid_warp_kernel(const KT* __restrict__ K, int64_t N, int B, int64_t total_blocks,
                      float* __restrict__ cent) {
     constexpr int L = D / 8, G = 32 / L, U = 8, W = 4;
     __shared__ float part[W][D];
@@ -112,25 +113,24 @@ centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int6
     const int j = (int)(wb - h * n_blocks);
     const int64_t t0 = (int64_t)j * B;
     const int len = (int)min64(B, N - t0);
-    const uint4* base = reinterpret_cast<const uint4*>(K + (h * N + t0) * D) + sub;
+    const KT* base = K + (h * N + t0) * D + sub * 8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int r0 = warp * G + grp; r0 < len; r0 += U * W * G) {
-        uint4 raw[U];
+        float x[U][8];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int r = r0 + u * W * G;
-            raw[u] = (r < len) ? __ldg(base + (int64_t)r * L) : make_uint4(0, 0, 0, 0);
-        }
+            if (r < len) {
+                ld8f(base + (int64_t)r * D, x[u]);
+            } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float2 f = unpack_bf16(w4[c]);
-                acc[2 * c] += f.x;
-                acc[2 * c + 1] += f.y;
+                for (int c = 0; c < 8; ++c) x[u][c] = 0.f;
             }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[c] += x[u][c];
     }
 #pragma unroll
     for (int o = L; o < 32; o <<= 1)
@@ -150,9 +150,9 @@ centroid_warp_kernel(const __nv_bfloat16* __restrict__ K, int64_t N, int B, int6
 // (head, block); a thread handles 8 channels of a row with 16-B loads of K
 // and its width-1 predecessors (L1 hits), writes K' (bf16) and accumulates
 // the unrounded fp32 K' for the centroid; fixed-order reduction.
-template <int D, int width>
+template <int D, int width, typename KT>
 __global__ void __launch_bounds__(128)
-centroid_conv_vec_kernel(const __nv_bfloat16* __restrict__ K, const float* __restrict__ W, int64_t N, int B,
+centroid_conv_vec_kernel(const KT* __restrict__ K, const float* __restrict__ W, int64_t N, int B,
                          __nv_bfloat16* __restrict__ Kout, float* __restrict__ cent) {
     constexpr int G = D / 8, RS = 128 / G;
     __shared__ float red[RS][D];
@@ -162,7 +162,7 @@ centroid_conv_vec_kernel(const __nv_bfloat16* __restrict__ K, const float* __res
     const int grp = threadIdx.x % G, rs = threadIdx.x / G;
     const int64_t t0 = (int64_t)j * B;
     const int len = (int)min64(B, N - t0);
-    const uint4* Kh = reinterpret_cast<const uint4*>(K + h * N * D);
+    const KT* Kh = K + h * N * D + grp * 8;
     uint4* Ko = reinterpret_cast<uint4*>(Kout + h * N * D);
     float w[width][8];
 #pragma unroll
@@ -172,27 +172,26 @@ centroid_conv_vec_kernel(const __nv_bfloat16* __restrict__ K, const float* __res
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int r = rs; r < len; r += RS) {
         const int64_t t = t0 + r;
-        uint4 raw[width];
-#pragma unroll
-        for (int l = 0; l < width; ++l) raw[l] = (t - l >= 0) ? __ldg(Kh + (t - l) * G + grp) : make_uint4(0, 0, 0, 0);
-        float x[8], a[8];
+        float xs[width][8];
 #pragma unroll
         for (int l = 0; l < width; ++l) {
-            const uint32_t v[4] = {raw[l].x, raw[l].y, raw[l].z, raw[l].w};
+            if (t - l >= 0) {
+                ld8f(Kh + (t - l) * D, xs[l]);
+            } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float2 f = unpack_bf16(v[c]);
-                if (l == 0) {
-                    x[2 * c] = f.x;
-                    x[2 * c + 1] = f.y;
-                    a[2 * c] = w[0][2 * c] * f.x;
-                    a[2 * c + 1] = w[0][2 * c + 1] * f.y;
-                } else {
-                    a[2 * c] = fmaf(w[l][2 * c], f.x, a[2 * c]);
-                    a[2 * c + 1] = fmaf(w[l][2 * c + 1], f.y, a[2 * c + 1]);
-                }
+                for (int c = 0; c < 8; ++c) xs[l][c] = 0.f;
             }
         }
+        float x[8], a[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            x[c] = xs[0][c];
+            a[c] = w[0][c] * xs[0][c];
+        }
+#pragma unroll
+        for (int l = 1; l < width; ++l)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) a[c] = fmaf(w[l][c], xs[l][c], a[c]);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             x[c] = x[c] + a[c] * sigmoidf_acc(a[c]);      // K' = K + silu(conv(K)) (src/keyconv.py:77-78)
@@ -419,6 +418,47 @@ __global__ void conv_dw_reduce_kernel(const float* __restrict__ dw_part, int64_t
     if (threadIdx.x == 0) dw[e] = red[0];
 }
 
+template <typename KT>
+static int run_centroids(const KT* k, const float* conv_w, int conv_width, int64_t bh, int64_t n_tokens,
+                         int head_dim, int block_size, void* k_conv_out, float* centroids, cudaStream_t s) {
+    if (bh < 1 || n_tokens < 1 || block_size < 1) return MOBA_ERR_SHAPE;
+    if (head_dim % 8 != 0 || head_dim > 256) return MOBA_ERR_UNSUPPORTED;
+    if (conv_width < 0 || conv_width > kMaxConv) return MOBA_ERR_CONFIG;
+    if (conv_width > 0 && (conv_w == nullptr || k_conv_out == nullptr)) return MOBA_ERR_CONFIG;
+    const int64_t n_blocks = ceil_div(n_tokens, block_size);
+    if (n_blocks > 2147483647 || bh > 65535) return MOBA_ERR_UNSUPPORTED;
+    StageTimer tm(T_CENTROID, s);
+    if (conv_width == 0 && (head_dim == 64 || head_dim == 128)) {
+        const int64_t total = bh * n_blocks;
+        if (head_dim == 64)
+            centroid_warp_kernel<64, KT><<<(unsigned)total, 128, 0, s>>>(k, n_tokens, block_size, total, centroids);
+        else
+            centroid_warp_kernel<128, KT><<<(unsigned)total, 128, 0, s>>>(k, n_tokens, block_size, total, centroids);
+        return check_launch("centroid_warp_kernel");
+    }
+    if (head_dim == 64 || head_dim == 128) {
+        using KernT = void (*)(const KT*, const float*, int64_t, int, __nv_bfloat16*, float*);
+        static const KernT k64[kMaxConv] = {centroid_conv_vec_kernel<64, 1, KT>, centroid_conv_vec_kernel<64, 2, KT>,
+                                            centroid_conv_vec_kernel<64, 3, KT>, centroid_conv_vec_kernel<64, 4, KT>,
+                                            centroid_conv_vec_kernel<64, 5, KT>};
+        static const KernT k128[kMaxConv] = {centroid_conv_vec_kernel<128, 1, KT>, centroid_conv_vec_kernel<128, 2, KT>,
+                                             centroid_conv_vec_kernel<128, 3, KT>, centroid_conv_vec_kernel<128, 4, KT>,
+                                             centroid_conv_vec_kernel<128, 5, KT>};
+        const KernT kern = head_dim == 64 ? k64[conv_width - 1] : k128[conv_width - 1];
+        kern<<<dim3((unsigned)n_blocks, (unsigned)bh), 128, 0, s>>>(k, conv_w, n_tokens, block_size,
+                                                                   (__nv_bfloat16*)k_conv_out, centroids);
+        return check_launch("centroid_conv_vec_kernel");
+    }
+    if constexpr (std::is_same<KT, __nv_bfloat16>::value) {
+        const int RG = kCentThreads / (head_dim / 8);
+        const size_t smem = (size_t)RG * head_dim * sizeof(float);
+        centroid_conv_kernel<<<dim3((unsigned)n_blocks, (unsigned)bh), kCentThreads, smem, s>>>(
+            k, conv_w, conv_width, n_tokens, head_dim, block_size, (__nv_bfloat16*)k_conv_out, centroids);
+        return check_launch("centroid_conv_kernel");
+    }
+    return MOBA_ERR_UNSUPPORTED;
+}
+
 }  // namespace moba
 
 using namespace moba;
@@ -426,43 +466,17 @@ using namespace moba;
 extern "C" int moba_centroids(const void* k, const float* conv_w, int conv_width, int64_t bh,
                               int64_t n_tokens, int head_dim, int block_size, void* k_conv_out,
                               float* centroids, void* stream) {
-    if (bh < 1 || n_tokens < 1 || block_size < 1) return MOBA_ERR_SHAPE;
-    if (head_dim % 8 != 0 || head_dim > 256) return MOBA_ERR_UNSUPPORTED;
-    if (conv_width < 0 || conv_width > kMaxConv) return MOBA_ERR_CONFIG;
-    if (conv_width > 0 && (conv_w == nullptr || k_conv_out == nullptr)) return MOBA_ERR_CONFIG;
-    const int64_t n_blocks = ceil_div(n_tokens, block_size);
-    if (n_blocks > 2147483647 || bh > 65535) return MOBA_ERR_UNSUPPORTED;
-    dim3 grid((unsigned)n_blocks, (unsigned)bh);
-    const int RG = kCentThreads / (head_dim / 8);
-    size_t smem = (size_t)RG * head_dim * sizeof(float);
-    StageTimer tm(T_CENTROID, (cudaStream_t)stream);
-    if (conv_width == 0 && (head_dim == 64 || head_dim == 128)) {
-        const int64_t total = bh * n_blocks;
-        if (head_dim == 64)
-            centroid_warp_kernel<64><<<(unsigned)total, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
-                                                                                      block_size, total, centroids);
-        else
-            centroid_warp_kernel<128><<<(unsigned)total, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, n_tokens,
-                                                                                       block_size, total, centroids);
-        return check_launch("centroid_warp_kernel");
-    }
-    if (head_dim == 64 || head_dim == 128) {
-        using KernT = void (*)(const __nv_bfloat16*, const float*, int64_t, int, __nv_bfloat16*, float*);
-        static const KernT k64[kMaxConv] = {centroid_conv_vec_kernel<64, 1>, centroid_conv_vec_kernel<64, 2>,
-                                            centroid_conv_vec_kernel<64, 3>, centroid_conv_vec_kernel<64, 4>,
-                                            centroid_conv_vec_kernel<64, 5>};
-        static const KernT k128[kMaxConv] = {centroid_conv_vec_kernel<128, 1>, centroid_conv_vec_kernel<128, 2>,
-                                             centroid_conv_vec_kernel<128, 3>, centroid_conv_vec_kernel<128, 4>,
-                                             centroid_conv_vec_kernel<128, 5>};
-        const KernT kern = head_dim == 64 ? k64[conv_width - 1] : k128[conv_width - 1];
-        kern<<<grid, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)k, conv_w, n_tokens, block_size,
-                                                     (__nv_bfloat16*)k_conv_out, centroids);
-        return check_launch("centroid_conv_vec_kernel");
-    }
-    centroid_conv_kernel<<<grid, kCentThreads, smem, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16*)k, conv_w, conv_width, n_tokens, head_dim, block_size,
-        (__nv_bfloat16*)k_conv_out, centroids);
-    return check_launch("centroid_conv_kernel");
+    clear_last_error();
+    return run_centroids((const __nv_bfloat16*)k, conv_w, conv_width, bh, n_tokens, head_dim, block_size, k_conv_out,
+                         centroids, (cudaStream_t)stream);
+}
+
+extern "C" int moba_centroids_f32(const float* k, const float* conv_w, int conv_width, int64_t bh,
+                                  int64_t n_tokens, int head_dim, int block_size, void* k_conv_out,
+                                  float* centroids, void* stream) {
+    clear_last_error();
+    return run_centroids(k, conv_w, conv_width, bh, n_tokens, head_dim, block_size, k_conv_out, centroids,
+                         (cudaStream_t)stream);
 }
 
 extern "C" size_t moba_conv_bwd_workspace_size(int64_t bh, int64_t n_tokens, int head_dim, int conv_width) {
@@ -472,6 +486,7 @@ extern "C" size_t moba_conv_bwd_workspace_size(int64_t bh, int64_t n_tokens, int
 extern "C" int moba_conv_bwd(const void* k, const float* conv_w, int conv_width, const void* dk_conv,
                              int64_t bh, int64_t n_tokens, int head_dim, void* dk, float* dw,
                              void* workspace, size_t workspace_bytes, void* stream) {
+    clear_last_error();
     if (bh < 1 || n_tokens < 1 || head_dim < 1) return MOBA_ERR_SHAPE;
     if (conv_width < 1 || conv_width > kMaxConv) return MOBA_ERR_CONFIG;
     if (workspace_bytes < moba_conv_bwd_workspace_size(bh, n_tokens, head_dim, conv_width))

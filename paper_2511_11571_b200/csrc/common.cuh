@@ -16,6 +16,8 @@ constexpr int kNumSMs = 148;
 
 // ---------------------------------------------------------------- status
 void set_last_error(const char* msg);
+// every exported entry point starts by clearing the previous call's message
+void clear_last_error();
 // checks cudaGetLastError after `n` kernel launches and counts them
 int check_launch(const char* what, int n = 1);
 
@@ -36,21 +38,6 @@ MOBA_DEV float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
-}
-
-// 2^x for x <= 0 on the FMA/ALU pipes (MUFU offload, as FlashAttention-4):
-// j = round(x) via the 1.5*2^23 magic add (no F2I / FRND, which would use the
-// same XU pipe as MUFU), f = x - j in [-0.5, 0.5], 2^f by a degree-3
-// relative-minimax polynomial (max rel. error 7.7e-5, far below bf16's
-// 2^-9), 2^j added to the exponent field. x is clamped at -126.
-MOBA_DEV float poly_exp2(float x) {
-    x = fmaxf(x, -126.f);
-    const float t = x + 12582912.0f;            // low mantissa bits = round(x)
-    const float f = x - (t - 12582912.0f);
-    float p = fmaf(0.05508876707445847f, f, 0.24260465620999191f);
-    p = fmaf(p, f, 0.6932762833525732f);
-    p = fmaf(p, f, 0.9999289048020072f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 // packed fp32x2 arithmetic (sm_100: one FFMA2 / FADD2 for two lanes of data)
@@ -77,6 +64,25 @@ MOBA_DEV uint32_t pack_bf16(float lo, float hi) {
 MOBA_DEV float2 unpack_bf16(uint32_t v) {
     __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&v);
     return __bfloat1622float2(h);
+}
+
+// 8 consecutive elements (bf16: one 16-B load; fp32: two) as fp32; the
+// fp32 forms serve numpy f32/f64 callers, whose Q / K are routed unrounded
+MOBA_DEV void ld8f(const __nv_bfloat16* p, float (&x)[8]) {
+    const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float2 f = unpack_bf16(u[c]);
+        x[2 * c] = f.x;
+        x[2 * c + 1] = f.y;
+    }
+}
+MOBA_DEV void ld8f(const float* p, float (&x)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
 
 // ---------------------------------------------------------------- smem / async copy
@@ -116,26 +122,6 @@ MOBA_DEV void cp_async16(uint32_t dst, const void* src, bool pred = true) {
 MOBA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 MOBA_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// ---------------------------------------------------------------- legacy tensor-core path
-MOBA_DEV void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-MOBA_DEV void ldmatrix_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-// D = A(16x16, row) * B(16x8, col) + D, bf16 inputs, fp32 accumulate.
-MOBA_DEV void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
-        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
 // fp32 vector reduction into global memory (no return value).
 MOBA_DEV void red_add_f32x2(float* addr, float a, float b) {

@@ -90,9 +90,9 @@ MOBA_DEV void select_chunk32(const float (&sv)[32], int j0, int lim, float (&ts)
     }
 }
 
-template <int D, int KMAX>
+template <int D, int KMAX, typename QT>
 __global__ void __launch_bounds__(kRouteThreads)
-route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, int64_t N,
+route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent, int64_t N,
                        int B, int top_k, int kv_group, int32_t* __restrict__ topk) {
     extern __shared__ __align__(16) float route_smem[];
     float (*q_s)[kRouteQ] = reinterpret_cast<float (*)[kRouteQ]>(route_smem);
@@ -106,7 +106,7 @@ route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restr
     const int64_t r0 = (int64_t)blockIdx.x * kRouteQ;
     const int n_blocks = (int)((N + B - 1) / B);
     const int width = top_k + 1;
-    const __nv_bfloat16* Qh = Q + h * N * D;
+    const QT* Qh = Q + h * N * D;
     const float* Ch = cent + (int64_t)(h / kv_group) * n_blocks * D;   // GQA: the query head's K/V head
 
     // stage the query tile transposed (fp32, exact)
@@ -114,16 +114,7 @@ route_topk_fp32_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restr
         int r = e / (D / 8), cg = e % (D / 8);
         int64_t i = r0 + r;
         float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (i < N) {
-            uint4 raw = *reinterpret_cast<const uint4*>(Qh + i * D + cg * 8);
-            const uint32_t* u = reinterpret_cast<const uint32_t*>(&raw);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float2 f = unpack_bf16(u[c]);
-                x[2 * c] = f.x;
-                x[2 * c + 1] = f.y;
-            }
-        }
+        if (i < N) ld8f(Qh + i * D + cg * 8, x);
 #pragma unroll
         for (int c = 0; c < 8; ++c) q_s[cg * 8 + c][r] = x[c];
     }
@@ -237,147 +228,9 @@ __global__ void centroid_split_kernel(const float* __restrict__ cent, int64_t to
 constexpr int kRtM = 128;   // queries per CTA (TMEM lanes)
 constexpr int kRtN = 64;    // centroids per chunk (MMA N)
 
-template <int D, int KMAX>
-__global__ void __launch_bounds__(128)
-route_topk_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
-                     int B, int top_k, int64_t split_rows, int kv_group, int32_t* __restrict__ topk) {
-    using namespace sm100;
-    constexpr int SL = D / 64;
-    constexpr uint32_t q_bytes = kRtM * D * 2;
-    constexpr uint32_t c_bytes = kRtN * D * 2;            // one split term of a chunk
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* q_s = smem;
-    uint8_t* c_s = q_s + q_bytes;                         // [2 buffers][3 terms][SL][128][128B]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(c_s + 2 * 3 * c_bytes);   // tma[2], mma[2]
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 4);
-    float* sel_s = reinterpret_cast<float*>(tmem_ptr + 4);                   // [4 warps][33][33]
-    int* sel_i = reinterpret_cast<int*>(sel_s + 4 * 33 * 33);
-
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t h = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * kRtM;
-    const int n_blocks = (int)((N + B - 1) / B);
-    const int width = top_k + 1;
-    const int64_t last_i = min64(r0 + kRtM, N) - 1;
-    const int max_own = (int)(last_i / B);
-    const int n_chunks = (max_own + kRtN - 1) / kRtN;
-
-    if (warp == 0) tmem_alloc(tmem_ptr, 2 * kRtN);
-    if (tid == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_ptr;
-    const uint32_t idesc = idesc_bf16(kRtM, kRtN, false, false);
-
-    auto load_chunk = [&](int c, int buf) {   // thread 0
-        mbar_expect_tx(&bars[buf], 3 * c_bytes + (c == 0 ? q_bytes : 0));
-        if (c == 0) {
-#pragma unroll
-            for (int sl = 0; sl < SL; ++sl)
-                tma_load_2d(smem_u32(q_s) + sl * kRtM * 128, &tm_q, sl * 64, (int)(h * N + r0), &bars[buf]);
-        }
-        const uint32_t cb = smem_u32(c_s) + buf * 3 * c_bytes;
-#pragma unroll
-        for (int term = 0; term < 3; ++term)
-#pragma unroll
-            for (int sl = 0; sl < SL; ++sl)
-                tma_load_2d(cb + term * c_bytes + sl * kRtN * 128, &tm_c, sl * 64,
-                            (int)(term * split_rows + (h / kv_group) * n_blocks + (int64_t)c * kRtN), &bars[buf]);
-    };
-    auto issue_mma = [&](int c) {             // thread 0
-        const int buf = c & 1;
-        mbar_wait(&bars[buf], (c >> 1) & 1);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(q_s), cb = smem_u32(c_s) + buf * 3 * c_bytes;
-        bool acc = false;
-#pragma unroll
-        for (int term = 0; term < 3; ++term)
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-                const int sl = kk >> 2, ke = (kk & 3) * 16;
-                umma_bf16(tmem + buf * kRtN, desc_kmajor(qa + sl * kRtM * 128, ke),
-                          desc_kmajor(cb + term * c_bytes + sl * kRtN * 128, ke), idesc, acc);
-                acc = true;
-            }
-        umma_commit(&bars[2 + buf]);
-    };
-
-    if (tid == 0 && n_chunks > 0) {
-        load_chunk(0, 0);
-        if (n_chunks > 1) load_chunk(1, 1);
-        issue_mma(0);
-    }
-
-    const int64_t my_i = r0 + tid;
-    const int my_own = (int)(min64(my_i, N - 1) / B);
-    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
-    float ts[KMAX];
-    int ti[KMAX];
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u) {
-        ts[u] = -INFINITY;
-        ti[u] = 0x7fffffff;
-    }
-    for (int c = 0; c < n_chunks; ++c) {
-        const int buf = c & 1;
-        mbar_wait(&bars[2 + buf], (c >> 1) & 1);        // S(c) in TMEM, smem buffer free
-        tc_fence_after();
-        if (tid == 0) {
-            if (c + 1 < n_chunks) issue_mma(c + 1);
-            if (c + 2 < n_chunks) load_chunk(c + 2, buf);
-        }
-        const int c0 = c * kRtN;
-        const int lim = min(kRtN, my_own - c0);          // strictly-past blocks only
-        const int lane = tid & 31;
-#pragma unroll 1
-        for (int k0 = 0; k0 < kRtN; k0 += 32) {
-            if (__all_sync(0xffffffffu, k0 >= lim)) break;       // rest of the chunk is not past for this warp
-            float sv[32];
-            tmem_ld32(tmem + buf * kRtN + lane_off + k0, sv);
-            tmem_ld_wait();
-            select_chunk32<KMAX>(sv, c0 + k0, (my_i < N) ? lim - k0 : 0, ts, ti, sel_s + lane + warp * 33 * 33,
-                                 sel_i + lane + warp * 33 * 33);
-        }
-        tc_fence_before();
-        __syncthreads();                                 // S buffer may be overwritten by MMA(c + 2)
-    }
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 2 * kRtN);
-    }
-    if (my_i >= N) return;
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u)
-        if (u >= top_k) ti[u] = 0x7fffffff;
-#pragma unroll
-    for (int p = 0; p < KMAX; ++p) {
-#pragma unroll
-        for (int u = (p & 1); u + 1 < KMAX; u += 2) {
-            int a = ti[u], b = ti[u + 1];
-            ti[u] = min(a, b);
-            ti[u + 1] = max(a, b);
-        }
-    }
-    int32_t* row = topk + (h * N + my_i) * width;
-    int nvalid = 0;
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u) {
-        if (ti[u] != 0x7fffffff) {
-            row[u] = ti[u];
-            ++nvalid;
-        }
-    }
-    row[nvalid] = my_own;
-    for (int s2 = nvalid + 1; s2 < width; ++s2) row[s2] = -1;
-}
-
 // ---------------------------------------------------------------- tensor-core routing, 2 threads per query
-// Same scores and selection order as route_topk_tc_kernel, but 8 warps per
+// Scores S = Q (C1 + C2 + C3)^T on tcgen05 (the bf16 hi/mid/lo split of the
+// fp32 centroids), the same selection order as route_topk_fp32_kernel; 8 warps per
 // CTA: the two warps of a TMEM lane quadrant split each 64-centroid chunk
 // (columns 0-31 / 32-63), each keeps its own running top-k of the query,
 // and the two lists (disjoint block sets, both ordered by score desc /
@@ -985,6 +838,28 @@ __global__ void validate_flat_kernel(const int32_t* __restrict__ counts, const i
     if (f) atomicOr(flags, f);
 }
 
+// bit5: every valid (query, block) entry of topk must appear in block's
+// slice. With the totals equal (bit3) and slices strictly ascending (bit4)
+// this makes the two layouts describe the same (query, block) set.
+__global__ void validate_membership_kernel(const int32_t* __restrict__ topk, const int32_t* __restrict__ counts,
+                                           const int32_t* __restrict__ offsets, const int32_t* __restrict__ flat,
+                                           int64_t N, int width, int n_blocks, int* __restrict__ flags) {
+    const int64_t h = blockIdx.y;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * width) return;
+    const int32_t b = topk[h * N * width + e];
+    if (b < 0) return;
+    const int32_t i = (int32_t)(e / width);
+    const int32_t* sl = flat + h * N * width + offsets[h * n_blocks + b];
+    const int c = counts[h * n_blocks + b];
+    int lo = 0, hi = c;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sl[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    if (lo >= c || sl[lo] != i) atomicOr(flags, 32);
+}
+
 // varlen workspace layout: [err int | cc int32 (bh * n_chunks * n)]
 struct VarlenGeom {
     int TQ;
@@ -1054,9 +929,18 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
 }
 
 template <int D, int KMAX>
-static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k, int mode,
-                        int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
+static int launch_route(const void* q, bool q_f32, const float* cent, int64_t bh, int64_t N, int B, int top_k,
+                        int mode, int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
     dim3 grid((unsigned)ceil_div(N, kRouteQ), (unsigned)bh);
+    const size_t fsmem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
+    if (q_f32) {
+        // fp32 queries (numpy f32 / f64 callers): exact fp32 products, no bf16 rounding before routing
+        if (mode != MOBA_ROUTE_FP32) return MOBA_ERR_CONFIG;
+        auto kern = route_topk_fp32_kernel<D, KMAX, float>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+        kern<<<grid, kRouteThreads, fsmem, s>>>((const float*)q, cent, N, B, top_k, kv_group, topk);
+        return check_launch("route_topk_fp32_kernel");
+    }
     if (mode == MOBA_ROUTE_TC) {
         const int64_t n = ceil_div(N, B);
         const int64_t bh_kv = bh / kv_group;
@@ -1069,41 +953,33 @@ static int launch_route(const void* q, const float* cent, int64_t bh, int64_t N,
         if (!make_tmap_bf16(&tm_q, q, (uint64_t)(bh * N), D, kRtM) ||
             !make_tmap_bf16(&tm_c, split, (uint64_t)(3 * bh_kv * n), D, kRtN))
             return MOBA_ERR_CUDA;
-        const char* impl = std::getenv("MOBA_ROUTE_IMPL");
-        if (impl != nullptr && impl[0] == '1') {
-            const size_t smem = 1024 + (size_t)kRtM * D * 2 + 2 * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 4 * 33 * 33 * 4;
-            auto kern = route_topk_tc_kernel<D, KMAX>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            kern<<<grid, 128, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, topk);
-            return check_launch("route_topk_tc_kernel");
-        }
         static_assert(kRtM * 64 * 2 + 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the Q + C buffers");
-        // one centroid buffer (3 CTAs per SM instead of 2) unless
-        // MOBA_ROUTE_CBUFS=2: measured 64K route 0.99 -> 0.86 ms
-        static const int cb_env = std::getenv("MOBA_ROUTE_CBUFS") ? std::atoi(std::getenv("MOBA_ROUTE_CBUFS")) : 1;
-        const int c_bufs = ceil_div(n - 1, kRtN) <= 1 ? 1 : (cb_env == 2 ? 2 : 1);
+        // one centroid buffer: 3 CTAs per SM instead of 2 (measured 64K
+        // route 0.99 -> 0.86 ms against two buffers)
+        const int c_bufs = 1;
         const size_t smem = 1024 + (size_t)kRtM * D * 2 + c_bufs * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
         auto kern = route_topk_tc2_kernel<D, KMAX>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, c_bufs, topk);
         return check_launch("route_topk_tc2_kernel");
     }
-    const size_t smem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
-    cudaFuncSetAttribute(route_topk_fp32_kernel<D, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    route_topk_fp32_kernel<D, KMAX><<<grid, kRouteThreads, smem, s>>>((const __nv_bfloat16*)q, cent, N, B,
-                                                                       top_k, kv_group, topk);
+    auto kern = route_topk_fp32_kernel<D, KMAX, __nv_bfloat16>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk);
     return check_launch("route_topk_fp32_kernel");
 }
 
 template <int D>
-static int dispatch_route_k(const void* q, const float* cent, int64_t bh, int64_t N, int B, int top_k, int mode,
-                            int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
-    if (top_k <= 1) return launch_route<D, 1>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
-    if (top_k <= 2) return launch_route<D, 2>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
-    if (top_k <= 4) return launch_route<D, 4>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
-    if (top_k <= 8) return launch_route<D, 8>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
-    if (top_k <= 16) return launch_route<D, 16>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
-    if (top_k <= 32) return launch_route<D, 32>(q, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s);
+static int dispatch_route_k(const void* q, bool q_f32, const float* cent, int64_t bh, int64_t N, int B, int top_k,
+                            int mode, int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
+#define MOBA_ROUTE_K(KM) launch_route<D, KM>(q, q_f32, cent, bh, N, B, top_k, mode, kv_group, topk, split_ws, s)
+    if (top_k <= 1) return MOBA_ROUTE_K(1);
+    if (top_k <= 2) return MOBA_ROUTE_K(2);
+    if (top_k <= 4) return MOBA_ROUTE_K(4);
+    if (top_k <= 8) return MOBA_ROUTE_K(8);
+    if (top_k <= 16) return MOBA_ROUTE_K(16);
+    if (top_k <= 32) return MOBA_ROUTE_K(32);
+#undef MOBA_ROUTE_K
     return MOBA_ERR_UNSUPPORTED;
 }
 
@@ -1123,10 +999,11 @@ extern "C" size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int bl
     return varlen_ws_bytes(bh, n_tokens, block_size) + 3 * (size_t)bh * ceil_div(n_tokens, block_size) * 128 * 2;
 }
 
-extern "C" int moba_route_gqa(const void* q, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
-                              int head_dim, int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
-                              int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
-                              size_t workspace_bytes, void* stream) {
+static int route_impl(const void* q, bool q_f32, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
+                      int head_dim, int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
+                      int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    clear_last_error();
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1) return MOBA_ERR_SHAPE;
     if (kv_group < 1 || bh % kv_group != 0) return MOBA_ERR_SHAPE;
     if (top_k < 1) return MOBA_ERR_CONFIG;
@@ -1139,14 +1016,32 @@ extern "C" int moba_route_gqa(const void* q, const float* centroids, int64_t bh,
     if (workspace_bytes < moba_route_workspace_size(bh, n_tokens, block_size, top_k)) return MOBA_ERR_WORKSPACE;
     void* split_ws = (char*)workspace + varlen_ws_bytes(bh, n_tokens, block_size);
     if (head_dim == 64)
-        st = dispatch_route_k<64>(q, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk, split_ws, s);
+        st = dispatch_route_k<64>(q, q_f32, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk,
+                                  split_ws, s);
     else if (head_dim == 128)
-        st = dispatch_route_k<128>(q, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk, split_ws, s);
+        st = dispatch_route_k<128>(q, q_f32, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk,
+                                   split_ws, s);
     else return MOBA_ERR_UNSUPPORTED;
     }
     if (st) return st;
     return run_varlen(topk, bh, n_tokens, top_k + 1, block_size, counts, offsets, flat, row_pos, workspace,
                       workspace_bytes, s, false);
+}
+
+extern "C" int moba_route_gqa(const void* q, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
+                              int head_dim, int block_size, int top_k, int mode, int32_t* topk, int32_t* counts,
+                              int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    return route_impl(q, false, centroids, bh, kv_group, n_tokens, head_dim, block_size, top_k, mode, topk, counts,
+                      offsets, flat, row_pos, workspace, workspace_bytes, stream);
+}
+
+extern "C" int moba_route_f32(const float* q, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
+                              int head_dim, int block_size, int top_k, int32_t* topk, int32_t* counts,
+                              int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    return route_impl(q, true, centroids, bh, kv_group, n_tokens, head_dim, block_size, top_k, MOBA_ROUTE_FP32, topk,
+                      counts, offsets, flat, row_pos, workspace, workspace_bytes, stream);
 }
 
 extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int64_t n_tokens, int head_dim,
@@ -1160,6 +1055,7 @@ extern "C" int moba_route(const void* q, const float* centroids, int64_t bh, int
 extern "C" int moba_varlen(const int32_t* topk, int64_t bh, int64_t n_tokens, int width, int block_size,
                            int32_t* counts, int32_t* offsets, int32_t* flat, int32_t* row_pos, void* workspace,
                            size_t workspace_bytes, void* stream) {
+    clear_last_error();
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
     if (width > 32) return MOBA_ERR_UNSUPPORTED;
     return run_varlen(topk, bh, n_tokens, width, block_size, counts, offsets, flat, row_pos, workspace,
@@ -1169,6 +1065,7 @@ extern "C" int moba_varlen(const int32_t* topk, int64_t bh, int64_t n_tokens, in
 extern "C" int moba_plan_row_pos(const int32_t* topk, const int32_t* counts, const int32_t* offsets,
                                  const int32_t* flat, int64_t bh, int64_t n_tokens, int width, int block_size,
                                  int32_t* row_pos, void* stream) {
+    clear_last_error();
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
     int n_blocks = (int)ceil_div(n_tokens, block_size);
     dim3 grid((unsigned)ceil_div(n_tokens * width, 256), (unsigned)bh);
@@ -1180,6 +1077,7 @@ extern "C" int moba_plan_row_pos(const int32_t* topk, const int32_t* counts, con
 extern "C" int moba_validate_plan(const int32_t* topk, const int32_t* counts, const int32_t* offsets,
                                   const int32_t* flat, int64_t bh, int64_t n_tokens, int width, int block_size,
                                   void* workspace, size_t workspace_bytes, void* stream) {
+    clear_last_error();
     if (bh < 1 || bh > 65535 || n_tokens < 1 || block_size < 1 || width < 1) return MOBA_ERR_SHAPE;
     size_t need = 256 + (size_t)bh * sizeof(unsigned long long);
     if (workspace_bytes < need) return MOBA_ERR_WORKSPACE;
@@ -1205,5 +1103,14 @@ extern "C" int moba_validate_plan(const int32_t* topk, const int32_t* counts, co
     cudaStreamSynchronize(s);
     st = check_launch("validate_flat_kernel");
     if (st) return st;
+    if (hf) return MOBA_ERR_PLAN;
+    // membership once the slices are known sorted and in range
+    validate_membership_kernel<<<dim3((unsigned)ceil_div(n_tokens * width, 256), (unsigned)bh), 256, 0, s>>>(
+        topk, counts, offsets, flat, n_tokens, width, n_blocks, flags);
+    cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    st = check_launch("validate_membership_kernel");
+    if (st) return st;
+    if (hf) set_last_error("a (query, block) entry of topk_indices is missing from its block's flat_queries slice");
     return hf ? MOBA_ERR_PLAN : MOBA_OK;
 }

@@ -36,7 +36,14 @@ class MobaGraphedStep:
             mk().requires_grad_(True), mk()
         self.conv_weight = None if conv_weight is None else conv_weight.detach().clone().requires_grad_(True)
         lib = _lib.load()
+        timing = lib.moba_timing_enabled()
         lib.moba_timing_enable(0)   # per-stage CUDA-event timers are not captured
+        try:
+            self._capture(dev, lib, warmup)
+        finally:
+            lib.moba_timing_enable(timing)
+
+    def _capture(self, dev, lib, warmup):
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _device
-from ._convert import from_heads, to_heads, to_weights
+from ._convert import from_heads, routing_heads, to_heads, to_weights
 from .core import ShapeError
 
 
@@ -54,8 +54,11 @@ def key_conv_forward(K, kernel: ConvKernel):
     if isinstance(K, np.ndarray) and K.ndim != 2:
         raise ShapeError("K must be 2-D (N x d)")
     k, info = to_heads(K, "K")
+    k32 = routing_heads(K, "K", device=k.device)       # conv of the unrounded keys; K' is rounded once
     w = to_weights(kernel.weights, info.d, info.dp, k.device)
-    _, k_conv = _device.centroids(k, min(256, info.n_tokens), w)
+    # the conv is fused with the centroid pass (moba_centroids); a block of
+    # 256 keys keeps that side output small
+    _, k_conv = _device.centroids(k if k32 is None else k32, min(256, info.n_tokens), w)
     return from_heads(k_conv, info)
 
 

@@ -132,8 +132,11 @@ class HostPipeline:
     def run(self, q, k, v, do, block_size, top_k, *, n_chunks=4, mode="tc", deterministic=False, out=None):
         """q, k, v, do: host bf16 tensors [H, N, d] (pinned for real overlap).
         Returns host (o, lse, dq, dk, dv); `out` may pass preallocated pinned
-        host buffers in that order. The call returns once every result is on
-        the host."""
+        host buffers in that order. The copies are asynchronous: the call
+        returns once they are enqueued and the current stream has been made to
+        wait for them, so the host buffers hold the results after
+        `torch.cuda.current_stream().synchronize()` (moba_fwd_bwd_host does
+        that unless synchronize=False)."""
         for name, t in (("q", q), ("k", k), ("v", v), ("do", do)):
             if t.is_cuda:
                 raise ShapeError(f"{name} must be a host tensor for the host pipeline")

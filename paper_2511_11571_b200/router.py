@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from ._convert import to_heads
+from ._convert import routing_heads, to_heads
 from .core import MobaConfig, OpCounters, PlanValidationError, RoutingPlan, ShapeError
 
 ROUTE_MODES = {"fp32": _lib.MOBA_ROUTE_FP32, "tc": _lib.MOBA_ROUTE_TC}
@@ -48,7 +48,8 @@ def compute_centroids(K, B: int, counters: OpCounters | None = None) -> Centroid
     if (isinstance(K, np.ndarray) and K.ndim != 2):
         raise ShapeError("K must be 2-D (N x d)")
     k, info = to_heads(K, "K")
-    cent, _ = _device.centroids(k, B)
+    k32 = routing_heads(K, "K", device=k.device)
+    cent, _ = _device.centroids(k if k32 is None else k32, B)
     if counters is not None:
         counters.bulk_elems += info.n_tokens * info.d + cent.shape[1] * info.d
     view = cent[..., : info.d]
@@ -68,7 +69,8 @@ def _route(Q, cents: CentroidMatrix, cfg: MobaConfig, counters, mode: str) -> tu
         raise ShapeError("centroids were not computed by this package for block_size_B")
     if cent.shape[0] != q.shape[0] or cent.shape[2] != q.shape[2]:
         raise ShapeError(f"centroid layout {tuple(cent.shape)} does not match Q {tuple(q.shape)}")
-    plan = _device.route(q, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])
+    q32 = routing_heads(Q, "Q", device=q.device) if mode == "fp32" else None
+    plan = _device.route(q if q32 is None else q32, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])
     if counters is not None:
         counters.score_flops += q.shape[0] * _device.scored_candidates(info.n_tokens, cfg.block_size_B) * info.d
     return plan, info
