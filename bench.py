@@ -3,26 +3,34 @@
 
 Contract (one JSON line on rank 0):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Under torchrun (N > 1) every rank runs its own heads (batch x heads shard
-over GPUs, no collective in the timed region; max-over-ranks timing).
 
-Workload (BASELINE.json configs[1]): per GPU 16 heads, N=8192, d=64, B=128,
-top-k 8, bf16 inputs resident in HBM; a "step" = centroids + top-k routing +
-varlen plan + forward + backward (given dO) over those heads. L2 (126 MB) is
-flushed between timed steps (the inputs are 16 MB each). Metric: MoBA
-fwd+bwd TFLOP/s with the reference's algorithmic FLOPs 14*d*P per head
-(P = visible (query, key) pairs, tests/oracles.py:95-98), plus ms/step.
+Workload = the metric's north-star point (BASELINE.json metric, paper Fig. 3
+shape): batch 2 x 16 heads, N = 64K, d = 64, B = 128,
+top-k 8, bf16 inputs resident in HBM (268 MB per tensor > the 126 MB L2;
+L2 is also flushed between timed steps). A step = centroids + top-k routing
+(tensor-core mode) + varlen plan + forward + backward (given dO), replayed as
+one CUDA graph (MobaGraphedStep). Metric: TFLOP/s with the reference's
+algorithmic FLOPs 14*d*P per head (P = visible (query, key) pairs,
+tests/oracles.py:95-98) plus ms/step.
 
---impl reference: the CPU oracle port (oracle/, the restatement of the
-reference's algorithm) on the box's host cores, one head per process,
-rank 0 only.
+N > 1 (torchrun): the FIXED 32-head set is sharded over the ranks by
+dist.shard_range (strong scaling, no collective in the timed region);
+after timing, O / LSE / dQ / dK / dV are all-gathered over NCCL and rank 0
+compares them with its own single-GPU run of all 32 heads.
+
+At N = 1 rank 0 adds `sweep`: N = 8K ... 512K at the same b2 x h16 shape,
+each point with MoBA ms / TFLOP/s, the dominant kernel's roofline and
+FlashAttention-2 dense fwd+bwd at the same shape.
+
+--impl reference: the unmodified reference package (baseline/_ref, its own
+public API moba_attention + moba_backward, src/attention.py:305, :239) on
+the host cores, rank 0 only.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -32,13 +40,14 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-HEADS, SEQ, DIM, BLOCK, TOPK = 16, 8192, 64, 128, 8
+BATCH, HEADS, SEQ, DIM, BLOCK, TOPK = 2, 16, 65536, 64, 128, 8
+SWEEP_N = (8192, 16384, 32768, 65536, 131072, 262144, 524288)
+REF_PREFIX = 16384      # reference-arm sample: the causal 16K-token prefix of a 64K head
 METRIC = "MoBA fwd+bwd ms and TFLOP/s vs seq len (B=128,k=8,d=64) vs FA2 dense & CPU ref"
 
 
 def visible_pairs(N, B, k):
-    # tests/oracles.py:95-98
-    full = N // B
+    # P = sum_i [min(k, i//B)*B + i%B + 1]  (tests/oracles.py:95-98)
     tot = 0
     for b in range(-(-N // B)):
         L = min(B, N - b * B)
@@ -50,6 +59,10 @@ def scored_candidates(N, B):
     return sum(min(B, N - b * B) * b for b in range(-(-N // B)))
 
 
+def plan_entries(N, B, k):
+    return sum(min(B, N - b * B) * (1 + min(k, b)) for b in range(-(-N // B)))
+
+
 def step_flops(H, N, d, B, k):
     return 14 * d * visible_pairs(N, B, k) * H
 
@@ -59,9 +72,19 @@ def load_peaks():
     try:
         with open(p) as f:
             j = json.load(f)
-        return j["hbm_gbs"], j["bf16_tflops"], j.get("bf16_tflops_sustained"), "measured"
+        return j["hbm_gbs"], j["bf16_tflops"], "MEASURED_PEAKS.json"
     except Exception:
-        return 6650.0, 1590.0, 1400.0, "fallback"
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ----------------------------------------------------------------- clocks
@@ -72,14 +95,12 @@ class ClockSampler:
 
     def __init__(self, device_index):
         self.samples = []
-        self.marks = []
         self.proc = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
                  "-i", str(device_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
@@ -122,7 +143,37 @@ class ClockSampler:
                 "samples": len(clocks), "window": window}
 
 
-# ----------------------------------------------------------------- reference arm (CPU oracle)
+# ----------------------------------------------------------------- reference (CPU) legs
+def _ref_module():
+    """The unmodified reference package shipped in baseline/_ref (pip
+    --target install of /root/reference/pkg); None if absent."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "moba")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import moba
+    return moba
+
+
+def _ref_head(args):
+    """One head through the reference's public API: moba_attention (routing +
+    forward, src/attention.py:305-314) then moba_backward (src/attention.py:
+    239-302), f32 inputs, single-threaded. Returns wall seconds."""
+    seed, N, d, B, k = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["MOBA_THREADS"] = "1"
+    import numpy as np
+    moba = _ref_module()
+    rng = np.random.default_rng(seed)
+    Q, K, V, dO = (rng.standard_normal((N, d)).astype(np.float32) for _ in range(4))
+    cfg = moba.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    t = time.perf_counter()
+    out, plan = moba.moba_attention(Q, K, V, cfg)
+    moba.moba_backward(Q, K, V, out.output, dO, out.logsumexp, plan, cfg)
+    return time.perf_counter() - t
+
+
 def _oracle_head(args):
     seed, N, d, B, k = args
     import numpy as np
@@ -136,45 +187,128 @@ def _oracle_head(args):
     return time.perf_counter() - t
 
 
-def cpu_oracle_run(n_heads, procs, N=SEQ, d=DIM, B=BLOCK, k=TOPK, seed0=0):
-    """Wall time of n_heads oracle fwd+bwd heads over `procs` worker processes."""
+def _pool_run(fn, jobs, procs):
     import multiprocessing as mp
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
-    os.environ["MKL_NUM_THREADS"] = "1"
+    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "MOBA_THREADS"):
+        os.environ[v] = "1"
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
-        pool.map(_oracle_head, [(seed0 + 1000 + i, 512, d, B, k) for i in range(procs)])  # warm imports
+        pool.map(fn, [(1000 + i, 512, DIM, BLOCK, TOPK) for i in range(procs)])   # warm imports
         t0 = time.perf_counter()
-        pool.map(_oracle_head, [(seed0 + i, N, d, B, k) for i in range(n_heads)])
+        pool.map(fn, jobs)
         return time.perf_counter() - t0
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    procs = max(1, min(os.cpu_count() or 1, HEADS))
-    per_head = step_flops(1, SEQ, DIM, BLOCK, TOPK)
-    for _ in range(max(0, args.warmup)):
-        cpu_oracle_run(procs, procs, seed0=7)
-    tot = 0.0
-    for s in range(args.steps):
-        tot += cpu_oracle_run(procs, procs, seed0=100 * s)
-    flops = per_head * procs * args.steps
+    moba = _ref_module()
+    fn, kind = (_ref_head, "reference") if moba is not None else (_oracle_head, "port")
+    H = BATCH * HEADS
+    procs = max(1, min(os.cpu_count() or 1, H))
+    N = REF_PREFIX
+    jobs = [(s, N, DIM, BLOCK, TOPK) for s in range(procs)]
+    import multiprocessing as mp
+    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "MOBA_THREADS"):
+        os.environ[v] = "1"
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        pool.map(fn, [(7 + i, 512, DIM, BLOCK, TOPK) for i in range(procs)])
+        for _ in range(max(0, args.warmup)):
+            pool.map(fn, jobs)
+        tot = 0.0
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(fn, jobs)
+            tot += time.perf_counter() - t0
+    flops = step_flops(procs, N, DIM, BLOCK, TOPK) * args.steps
     value = flops / tot / 1e12
+    sample = (f"per step: {procs} heads (one per process) of the workload's causal {N}-token prefix "
+              f"(queries 0..{N - 1} attend only keys < {N}, an exact sub-problem of each 64K head), "
+              f"d={DIM} B={BLOCK} k={TOPK}, f32, through the reference's moba_attention + moba_backward "
+              f"({'baseline/_ref' if kind == 'reference' else 'oracle port: baseline/_ref missing'}); "
+              f"the reference's select_topk grows as N^2/B, so its prefix rate overstates its full-64K rate")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3 * HEADS / procs,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "configs[1]: 16 heads x N=8192, d=64, B=128, top-k 8, routing+fwd+bwd",
-                   "parallelism": f"cpu x{procs} processes"},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} heads (one per process) of N={SEQ} d={DIM} B={BLOCK} k={TOPK}, "
-                                   f"numpy f64 oracle (oracle/moba_oracle.py), OPENBLAS_NUM_THREADS=1, "
-                                   f"per step; ms_per_step scaled to 16 heads"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"b{BATCH} x h{HEADS}, N={SEQ}, d={DIM}, B={BLOCK}, top-k {TOPK}: routing + fwd + bwd "
+                               f"(timed on a bounded sample, see cpu_baseline.sample)",
+                   "parallelism": f"cpu x{procs} processes", "cpu_model": cpu_model()},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": procs, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_single_head():
+    """One full 64K head of the workload through the reference on one core
+    (~20 s): the reference's true per-head rate at the headline point."""
+    moba = _ref_module()
+    fn, kind = (_ref_head, "reference") if moba is not None else (_oracle_head, "port")
+    wall = _pool_run(fn, [(0, SEQ, DIM, BLOCK, TOPK)], 1)
+    return {"value": step_flops(1, SEQ, DIM, BLOCK, TOPK) / wall / 1e12, "unit": "TFLOP/s", "cores": 1,
+            "kind": kind, "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+            "sample": f"one full head of the workload (N={SEQ}, d={DIM}, B={BLOCK}, k={TOPK}), f32, "
+                      f"{'reference moba_attention + moba_backward (baseline/_ref)' if kind == 'reference' else 'f64 oracle port'}"
+                      f", single core: {wall:.1f} s (the workload has {BATCH * HEADS} heads)"}
+
+
+# ----------------------------------------------------------------- GPU arm helpers
+def time_graph(gs, steps, flush, stream=None):
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()                       # evict L2 between steps (untimed)
+        evs[i][0].record()
+        gs.replay()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def stage_profile(mb, lib, _lib, q, k, v, do, B, topk, mode, flush, reps=2):
+    """Per-stage device time of eager steps (CUDA-event stage timers on the
+    launching stream inside libmoba_b200.so): {stage: (ms per launch, launches per step)}."""
+    import torch
+    qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, k, v))
+    torch.cuda.synchronize()
+    lib.moba_timing_reset()
+    lib.moba_timing_enable(1)
+    for _ in range(reps):
+        flush.zero_()
+        for t in (qg, kg, vg):
+            t.grad = None
+        out = mb.moba_attn(qg, kg, vg, B, topk, mode=mode)
+        out.backward(do)
+    torch.cuda.synchronize()
+    st = _lib.timing_read()
+    lib.moba_timing_enable(0)
+    return {s: (ms / max(n, 1), n / reps) for s, (ms, n) in st.items() if n > 0}
+
+
+def roofline_of(stages, H, N, d, B, k, hbm, tc_peak, peak_src):
+    """Dominant kernel's achieved rate vs its roofline. Algorithmic work per
+    launch (one launch covers the rank's H heads):
+    fwd 4dP, bwd 10dP, route 2dR FLOP; combine / centroid bytes."""
+    P, R, E = visible_pairs(N, B, k), scored_candidates(N, B), plan_entries(N, B, k)
+    n = -(-N // B)
+    algo = {
+        "fwd": ("tensor", 4 * d * P * H / 1e12, "TFLOP/s"),
+        "bwd": ("tensor", 10 * d * P * H / 1e12, "TFLOP/s"),
+        "route": ("tensor", 2 * d * R * H / 1e12, "TFLOP/s"),
+        "combine": ("hbm", H * (E * (2 * d + 4) + N * (k + 1) * 4 + N * (2 * d + 4)) / 1e9, "GB/s"),
+        "centroid": ("hbm", H * (2 * N * d + 4 * n * d) / 1e9, "GB/s"),
+    }
+    dom = max((s for s in stages if s in algo), key=lambda s: stages[s][0] * stages[s][1])
+    bound, work, unit = algo[dom]
+    avg_ms = stages[dom][0]
+    achieved = work / (avg_ms / 1e3)
+    peak = tc_peak if bound == "tensor" else hbm
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "kernel": dom, "avg_ms": avg_ms,
+            "peak_source": f"{peak_src} ({'bf16 dense burst' if bound == 'tensor' else 'HBM copy'})",
+            "stage_ms_per_step": {s: round(v[0] * v[1], 4) for s, v in stages.items()}}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -184,105 +318,82 @@ def run_ours(args, rank, world):
 
     import paper_2511_11571_b200 as mb
     from paper_2511_11571_b200 import _lib
+    from paper_2511_11571_b200.dist import gather_and_compare, shard_range
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     lib = _lib.load()
-    H, N, d, B, k = HEADS, SEQ, DIM, BLOCK, TOPK
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q, kk, v, do = (torch.randn(H, N, d, generator=gen, device=dev).bfloat16() for _ in range(4))
-    qg, kg, vg = (t.detach().clone().requires_grad_(True) for t in (q, kk, v))
+    Hg, N, d, B, k = BATCH * HEADS, SEQ, DIM, BLOCK, TOPK
+    lo, hi = shard_range(Hg, world, rank)
+    H = hi - lo
+    gen = torch.Generator(device=dev).manual_seed(1234)        # the same global inputs on every rank
+    full = [torch.randn(Hg, N, d, generator=gen, device=dev).bfloat16() for _ in range(4)]
+    q, kk, v, do = (t[lo:hi].contiguous() for t in full)
+    if world == 1:
+        del full
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    def step(qx, kx, vx, dox):
-        for t in (qx, kx, vx):
-            t.grad = None
-        out = mb.moba_attn(qx, kx, vx, B, k, mode=args.route_mode, deterministic=args.deterministic)
-        out.backward(dox)
-        return out
-
+    # ---- the step captured once as a CUDA graph (MobaGraphedStep, the public
+    # API for fixed-shape training loops) and replayed
+    gs = mb.MobaGraphedStep((H, N, d), B, k, mode=args.route_mode, deterministic=args.deterministic)
+    gs.step(q, kk, v, do)
     for _ in range(args.warmup):
-        step(qg, kg, vg, do)
+        gs.replay()
     torch.cuda.synchronize()
-
     sampler = ClockSampler(dev.index) if rank == 0 else None
     time.sleep(0.3 if sampler else 0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    lib.moba_timing_reset()
-    lib.moba_timing_enable(1)
-    launches0 = lib.moba_launch_count()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_wall0 = time.time()
-    for i in range(args.steps):
-        flush.zero_()                       # evict L2 between steps (untimed)
-        evs[i][0].record()
-        step(qg, kg, vg, do)
-        evs[i][1].record()
-    torch.cuda.synchronize()
-    t_wall1 = time.time()
+    t0 = time.time()
+    ms_list = time_graph(gs, args.steps, flush)
+    t1 = time.time()
     if world > 1:
         dist.barrier()
-    launches = int(lib.moba_launch_count() - launches0)
-    stages = _lib.timing_read()
-    lib.moba_timing_enable(0)
-    ms = sum(a.elapsed_time(b) for a, b in evs)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    ms = torch.tensor([sum(ms_list)], device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_max = float(ms.item())
     clocks = None
     if sampler:
         time.sleep(0.25)
         sampler.stop()
-        clocks = sampler.summary(t_wall0, t_wall1)
+        clocks = sampler.summary(t0, t1)
+    launches = gs.launches_per_step * args.steps
+    flops_job = step_flops(Hg, N, d, B, k)
+    value = flops_job * args.steps / (ms_max / 1e3) / 1e12
 
-    flops_rank = step_flops(H, N, d, B, k)
-    eager_ms = ms_max
-    eager_value = flops_rank * world * args.steps / (eager_ms / 1e3) / 1e12
+    # ---- multi-GPU verification (after timing): gather every rank's shard
+    # over NCCL and compare with rank 0's single-GPU run of all heads
+    verify = None
+    if world > 1:
+        local = {"O": gs.out.detach(), "LSE": gs.lse.detach(), "dQ": gs.q.grad, "dK": gs.k.grad, "dV": gs.v.grad}
+        ref = None
+        if rank == 0:
+            xs = [t.clone().requires_grad_(True) for t in full[:3]]
+            o, l = mb.moba_attn(*xs, B, k, mode=args.route_mode, deterministic=args.deterministic, return_lse=True)
+            o.backward(full[3])
+            ref = {"O": o.detach(), "LSE": l.detach(), "dQ": xs[0].grad, "dK": xs[1].grad, "dV": xs[2].grad}
+        res = gather_and_compare(local, ref, Hg, dev)
+        if rank == 0:
+            verify = {nm: {"bitwise": b, "max_abs": m} for nm, (b, m) in res.items()}
+            verify["note"] = ("O, LSE, dK, dV are deterministic kernels (bitwise); dQ under the parallel "
+                              "schedule uses fp32 reduction atomics (order-dependent rounding)"
+                              if not args.deterministic else "deterministic schedule: all bitwise")
+        del full
+    # ---- fp32-mode routing (the bit-exact parity router) timed beside the headline
+    fp32_route = None
+    if rank == 0 and args.route_mode == "tc" and not args.no_extra:
+        g32 = mb.MobaGraphedStep((H, N, d), B, k, mode="fp32", deterministic=args.deterministic)
+        g32.step(q, kk, v, do)
+        g32.replay()
+        t32 = time_graph(g32, max(3, min(args.steps, 10)), flush)
+        fp32_route = {"ms_per_step": sum(t32) / len(t32),
+                      "value": step_flops(H, N, d, B, k) / (sum(t32) / len(t32) / 1e3) / 1e12}
+        del g32
 
-    # ---- the same step replayed as one CUDA graph (MobaGraphedStep: the
-    # public API for fixed-shape training loops); this is the headline value
-    graph_info = None
-    if not args.no_graph:
-        gs = mb.MobaGraphedStep((H, N, d), B, k, mode=args.route_mode, deterministic=args.deterministic)
-        gs.step(q, kk, v, do)
-        for _ in range(args.warmup):
-            gs.replay()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        gevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        sampler_g = ClockSampler(dev.index) if rank == 0 else None
-        time.sleep(0.3 if sampler_g else 0)
-        tg0 = time.time()
-        for i in range(args.steps):
-            flush.zero_()
-            gevs[i][0].record()
-            gs.replay()
-            gevs[i][1].record()
-        torch.cuda.synchronize()
-        tg1 = time.time()
-        gms = torch.tensor([sum(a.elapsed_time(b) for a, b in gevs)], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(gms, op=dist.ReduceOp.MAX)
-        if sampler_g:
-            time.sleep(0.25)
-            sampler_g.stop()
-            clocks = sampler_g.summary(tg0, tg1)
-        # parity of the replay against the eager step (same inputs)
-        out_e = mb.moba_attn(q, kk, v, B, k, mode=args.route_mode)
-        graph_info = {"ms_per_step": float(gms.item()) / args.steps,
-                      "launches_per_step": gs.launches_per_step,
-                      "max_abs_vs_eager_out": float((gs.out.float() - out_e.float()).abs().max().item())}
-        ms_max = float(gms.item())
-        launches = gs.launches_per_step * args.steps
-        del gs
-    value = flops_rank * world * args.steps / (ms_max / 1e3) / 1e12
-
-    # ---- end to end through the public host-buffer API: pinned host Q, K, V, dO
-    # in, host O, LSE, dQ, dK, dV out; heads pipelined over copy/compute streams
+    # ---- end to end through the public host-buffer API: pinned host Q, K,
+    # V, dO in, host O, LSE, dQ, dK, dV out (copies inside the timed region)
     pin = [t.cpu().pin_memory() for t in (q, kk, v, do)]
     outs_h = (torch.empty((H, N, d), dtype=torch.bfloat16).pin_memory(),
               torch.empty((H, N), dtype=torch.float32).pin_memory(),
@@ -301,72 +412,57 @@ def run_ours(args, rank, world):
     te = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = flops_rank * world * args.steps / (float(te.item()) / 1e3) / 1e12
+    e2e_val = flops_job * args.steps / (float(te.item()) / 1e3) / 1e12
     h2d_bytes = sum(t.numel() * t.element_size() for t in pin)
     d2h_bytes = sum(t.numel() * t.element_size() for t in outs_h)
+    del pin, outs_h
 
-    if rank != 0:
-        return
-
-    # ---- roofline of the dominant kernel (stage timers, same timed region)
-    hbm, tc_burst, tc_sus, peak_kind = load_peaks()
-    P = visible_pairs(N, B, k)
-    R = scored_candidates(N, B)
-    E = sum(1 + min(k, i // B) for i in range(0, N))
-    algo = {  # algorithmic work per launch (one launch covers all H heads)
-        "fwd": ("tensor", 4 * d * P * H / 1e12, "TFLOP/s"),
-        "bwd": ("tensor", 10 * d * P * H / 1e12, "TFLOP/s"),
-        "route": ("tensor", 2 * d * R * H / 1e12, "TFLOP/s"),
-        "combine": ("hbm", H * (E * (2 * d + 4) + N * (k + 1) * 4 + N * (2 * d + 4)) / 1e9, "GB/s"),
-        "centroid": ("hbm", H * (2 * N * d + 4 * (-(-N // B)) * d) / 1e9, "GB/s"),
-    }
-    stage_ms = {s: (v_[0] / max(v_[1], 1), v_[1]) for s, v_ in stages.items() if v_[1] > 0}
-    dom = max((s for s in stage_ms if s in algo), key=lambda s: stage_ms[s][0] * stage_ms[s][1])
-    bound, work, unit = algo[dom]
-    avg_ms = stage_ms[dom][0]
-    achieved = work / (avg_ms / 1e3)
-    peak = tc_burst if bound == "tensor" else hbm
-    traffic = None
+    # ---- roofline of the dominant kernel: per-stage device time measured on
+    # the launching stream (library stage timers) in eager steps right after
+    hbm, tc_peak, peak_src = load_peaks()
+    stages = stage_profile(mb, lib, _lib, q, kk, v, do, B, k, args.route_mode, flush)
+    roofline = roofline_of(stages, H, N, d, B, k, hbm, tc_peak, peak_src)
+    roofline["traffic"] = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dom)
+            tj = json.load(open(tp))
+            if tj.get("workload") == f"b{BATCH}h{HEADS}_n{N}_d{d}" and world == 1:
+                roofline["traffic"] = tj.get(roofline["kernel"])
+                roofline["traffic_source"] = tj.get("source")
         except Exception:
-            traffic = None
-    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "traffic": traffic, "kernel": dom, "avg_ms": avg_ms,
-                "peak_source": f"MEASURED_PEAKS.json ({peak_kind}, burst)" if bound == "tensor"
-                else f"MEASURED_PEAKS.json ({peak_kind})",
-                "stage_ms_per_step": {s: round(v_[0] * v_[1] / args.steps, 4) for s, v_ in stage_ms.items()}}
+            pass
+    if rank != 0:
+        return
+    del gs, q, kk, v, do
+    torch.cuda.empty_cache()
 
-    # ---- CPU baseline (oracle port) and FA2 dense comparator
     cpu = None
     if world == 1 and not args.no_cpu:
-        procs = max(1, min(os.cpu_count() or 1, H))
-        wall = cpu_oracle_run(procs, procs)
-        cpu = {"value": step_flops(1, N, d, B, k) * procs / wall / 1e12, "unit": "TFLOP/s", "cores": procs,
-               "kind": "port",
-               "sample": f"{procs} heads (one per process) of configs[1] (N={N}, d={d}, B={B}, k={k}) "
-                         f"routing+fwd+bwd in the f64 numpy oracle, {wall:.1f} s wall"}
-    extra = {}
-    if not args.no_extra:
-        extra = extra_measurements(args, dev, mb, flush)
+        cpu = cpu_baseline_single_head()
+    sweep = None
+    if world == 1 and not args.no_extra:
+        sweep = run_sweep(args, dev, mb, lib, _lib, flush, hbm, tc_peak, peak_src,
+                          headline={"N": N, "moba_ms": ms_max / args.steps, "roofline": roofline})
 
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, seeded per rank)",
-        "config": {"workload": f"configs[1]: {H} heads/GPU x N={N}, d={d}, B={B}, top-k {k}; step = centroids + "
-                               f"top-k routing ({args.route_mode}) + varlen + fwd + bwd"
-                               + (", replayed as one CUDA graph (MobaGraphedStep)" if graph_info else ", eager"),
-                   "submission": "cuda_graph" if graph_info else "eager",
-                   "eager": {"ms_per_step": eager_ms / args.steps, "value": eager_value},
-                   "graph": graph_info,
-                   "heads_per_gpu": H, "seq_len": N, "head_dim": d, "block_size": B, "top_k": k,
-                   "parallelism": f"heads sharded over {world} GPU(s), no collective",
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (torch.randn, seed 1234, the same global inputs on every rank)",
+        "config": {"workload": f"metric north-star point: b{BATCH} x h{HEADS} = {Hg} heads, N={N}, d={d}, B={B}, "
+                               f"top-k {k}; step = centroids + top-k routing ({args.route_mode}) + varlen + fwd + "
+                               f"bwd, replayed as one CUDA graph (MobaGraphedStep)",
+                   "batch": BATCH, "heads": HEADS, "seq_len": N, "head_dim": d, "block_size": B, "top_k": k,
+                   "heads_per_gpu": H, "submission": "cuda_graph",
+                   "parallelism": f"{Hg} heads sharded over {world} GPU(s) (dist.shard_range), no collective "
+                                  f"in the timed region",
                    "bwd_schedule": "deterministic" if args.deterministic else "parallel",
-                   "l2": "flushed (512 MB write) between timed steps",
-                   "flops_per_step_per_gpu": flops_rank},
+                   "route_mode": args.route_mode,
+                   "fp32_route_step": fp32_route,
+                   "l2": "flushed (512 MB write) between timed steps; inputs 268 MB per tensor exceed L2",
+                   "flops_per_step": flops_job, "launches_per_step": launches // max(args.steps, 1),
+                   "multi_gpu_verify": verify},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d_bytes,
@@ -375,7 +471,7 @@ def run_ours(args, rank, world):
                         f"H2D / one CUDA-graph replay per chunk / D2H on 3 streams) -> host O,LSE,dQ,dK,dV"},
         "gpu_launches": launches,
         "clocks": clocks,
-        "extra": extra,
+        "sweep": sweep,
     }
     print(json.dumps(line), flush=True)
 
@@ -395,34 +491,46 @@ def time_cuda(fn, reps, flush):
     return tot[len(tot) // 2]
 
 
-def extra_measurements(args, dev, mb, flush):
-    """FA2 dense at the headline shape and the north-star point (N=64K,
-    b2 x h16, d=64, B=128, k=8) for MoBA and FA2."""
+def run_sweep(args, dev, mb, lib, _lib, flush, hbm, tc_peak, peak_src, headline):
+    """The metric's sequence-length sweep (paper Fig. 3: bsz 2, B=128, k=8;
+    here 16 heads, d=64): per N the graphed MoBA step (median of reps), the
+    dominant kernel's roofline, and FA2 dense fwd+bwd at the same shape."""
     import torch
-    out = {}
     try:
         from flash_attn import flash_attn_func
-    except Exception as e:  # pragma: no cover
+    except Exception:  # pragma: no cover
         flash_attn_func = None
-        out["fa2_error"] = str(e)[:200]
-    for tag, H, N in (("n8k_h16", HEADS, SEQ), ("n64k_b2h16", 32, 65536)):
+    Hg, d, B, k = BATCH * HEADS, DIM, BLOCK, TOPK
+    points = []
+    for N in SWEEP_N:
+        if args.sweep_max and N > args.sweep_max:
+            break
         gen = torch.Generator(device=dev).manual_seed(7)
-        q, kk, v, do = (torch.randn(H, N, DIM, generator=gen, device=dev).bfloat16() for _ in range(4))
-        qg, kg, vg = (t.clone().requires_grad_(True) for t in (q, kk, v))
-
-        def moba():
-            for t in (qg, kg, vg):
-                t.grad = None
-            o = mb.moba_attn(qg, kg, vg, BLOCK, TOPK, mode=args.route_mode)
-            o.backward(do)
-
-        moba()
-        reps = 5 if N > 16384 else 10
-        ms = time_cuda(moba, reps, flush)
-        rec = {"moba_ms": ms, "moba_tflops": step_flops(H, N, DIM, BLOCK, TOPK) / (ms / 1e3) / 1e12}
-        if flash_attn_func is not None:
-            qf, kf, vf = (t.transpose(0, 1).unsqueeze(0).contiguous().requires_grad_(True) for t in (q, kk, v))
-            dof = do.transpose(0, 1).unsqueeze(0).contiguous()
+        q, kk, v, do = (torch.randn(Hg, N, d, generator=gen, device=dev).bfloat16() for _ in range(4))
+        rec = {"N": N}
+        if N == headline["N"]:
+            rec["moba_ms"] = headline["moba_ms"]
+            roof = headline["roofline"]
+        else:
+            gs = mb.MobaGraphedStep((Hg, N, d), B, k, mode=args.route_mode)
+            gs.step(q, kk, v, do)
+            gs.replay()
+            reps = 5 if N >= 131072 else 10
+            t = sorted(time_graph(gs, reps, flush))
+            rec["moba_ms"] = t[len(t) // 2]
+            del gs
+            torch.cuda.empty_cache()
+            roof = roofline_of(stage_profile(mb, lib, _lib, q, kk, v, do, B, k, args.route_mode, flush, reps=1),
+                               Hg, N, d, B, k, hbm, tc_peak, peak_src)
+        rec["moba_tflops"] = step_flops(Hg, N, d, B, k) / (rec["moba_ms"] / 1e3) / 1e12
+        rec["dominant"] = {x: roof[x] for x in ("kernel", "bound", "achieved", "unit", "frac", "avg_ms")}
+        rec["stage_ms_per_step"] = roof["stage_ms_per_step"]
+        if flash_attn_func is not None and not args.no_fa2:
+            qf, kf, vf = (t.view(BATCH, HEADS, N, d).transpose(1, 2).contiguous().requires_grad_(True)
+                          for t in (q, kk, v))
+            dof = do.view(BATCH, HEADS, N, d).transpose(1, 2).contiguous()
+            del q, kk, v, do
+            torch.cuda.empty_cache()
 
             def fa2():
                 for t in (qf, kf, vf):
@@ -431,15 +539,17 @@ def extra_measurements(args, dev, mb, flush):
                 o.backward(dof)
 
             fa2()
-            fms = time_cuda(fa2, 3 if N > 16384 else 10, flush)
-            dense = 14 * DIM * N * (N + 1) // 2 * H
+            fms = time_cuda(fa2, 2 if N >= 262144 else (3 if N >= 65536 else 10), flush)
+            dense = 14 * d * N * (N + 1) // 2 * Hg
             rec.update({"fa2_dense_ms": fms, "fa2_dense_tflops": dense / (fms / 1e3) / 1e12,
-                        "speedup_vs_fa2": fms / ms})
+                        "speedup_vs_fa2": fms / rec["moba_ms"]})
             del qf, kf, vf, dof
-        out[tag] = rec
-        del q, kk, v, do, qg, kg, vg
+        points.append(rec)
         torch.cuda.empty_cache()
-    return out
+    return {"shape": f"b{BATCH} x h{HEADS}, d={d}, B={B}, top-k {k}, routing ({args.route_mode}) + fwd + bwd",
+            "fa2": "flash_attn.flash_attn_func(causal=True) fwd+bwd, bf16 [b, N, h, d], median of reps, "
+                   "FLOPs 14*d*N(N+1)/2 per head",
+            "points": points}
 
 
 def main():
@@ -452,10 +562,12 @@ def main():
     ap.add_argument("--deterministic", action="store_true", help="deterministic dQ schedule")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="head chunks of the host-buffer pipeline")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extra", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="headline from eager launches instead of a CUDA graph")
+    ap.add_argument("--no-extra", action="store_true", help="skip the sweep and the fp32-route step")
+    ap.add_argument("--no-fa2", action="store_true")
+    ap.add_argument("--sweep-max", type=int, default=0, help="largest N of the sweep (0 = 512K)")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":

@@ -39,6 +39,9 @@ __all__ = [
     "forward",
     "backward",
     "attention",
+    "forward_rows",
+    "backward_rows_dq",
+    "backward_block",
     "visible_pairs",
     "plan_entries",
     "scored_candidates",
@@ -349,3 +352,69 @@ def attention(Q, K, V, B: int, k: int, conv_W=None):
     plan = build_plan(Q, Kf, B, k)
     O, L = forward(Q, Kf, V, plan, B)
     return O, L, plan, Kf
+
+
+# --------------------------------------------------------------------------
+# row / block restrictions of forward and backward, for sampled checks at
+# sizes where the whole-head oracle is too slow (512K): the same algebra as
+# forward / backward above, restricted to chosen query rows or key blocks
+# --------------------------------------------------------------------------
+
+def _row_keys(i: int, blocks, B: int, N: int):
+    """Visible keys of query i over its plan blocks: whole blocks, own block
+    up to i (token-causal mask key > query, src/attention.py:127-133)."""
+    ks = [np.arange(j * B, min(j * B + B, N, i + 1)) for j in blocks if j >= 0]
+    return np.concatenate(ks) if ks else np.zeros(0, dtype=np.int64)
+
+
+def forward_rows(Q, K, V, rows, topk_rows, B: int):
+    """O [r, d], LSE [r] for the query rows `rows` given their plan rows
+    (topk_rows [r, width], -1 tail): one softmax over all visible keys of the
+    row's blocks, equal to merging the per-block partials
+    (SoftmaxState.update/finalize, src/attention.py:60-74)."""
+    Q, K, V = (np.asarray(x, dtype=np.float64) for x in (Q, K, V))
+    N, d = Q.shape
+    scale = 1.0 / np.sqrt(d)
+    O = np.zeros((len(rows), d))
+    L = np.zeros(len(rows))
+    for r, i in enumerate(rows):
+        ks = _row_keys(int(i), topk_rows[r], B, N)
+        s = (Q[i] * scale) @ K[ks].T
+        m = s.max()
+        p = np.exp(s - m)
+        O[r] = p @ V[ks] / p.sum()
+        L[r] = m + np.log(p.sum())
+    return O, L
+
+
+def backward_rows_dq(Q, K, V, O_rows, dO, L_rows, rows, topk_rows, B: int):
+    """dQ rows: dQ_i = scale * sum_k P_ik (dP_ik - D_i) K_k with P = exp(S -
+    L), dP = dO V^T, D_i = dO_i . O_i (src/attention.py:229-234, :266,
+    :299)."""
+    Q, K, V, dO = (np.asarray(x, dtype=np.float64) for x in (Q, K, V, dO))
+    N, d = Q.shape
+    scale = 1.0 / np.sqrt(d)
+    dQ = np.zeros((len(rows), d))
+    for r, i in enumerate(rows):
+        ks = _row_keys(int(i), topk_rows[r], B, N)
+        P = np.exp((Q[i] * scale) @ K[ks].T - L_rows[r])
+        dS = P * (dO[i] @ V[ks].T - dO[i] @ O_rows[r])
+        dQ[r] = scale * (dS @ K[ks])
+    return dQ
+
+
+def backward_block(Q, K, V, dO, j: int, queries, O_q, L_q, B: int):
+    """(dK_j, dV_j) [len_j, d] of key block j from the queries attending it
+    (its flat slice) with their O and LSE: dV_j = P^T dO, dK_j = dS^T
+    Q_scaled (src/attention.py:230-233)."""
+    Q, K, V, dO = (np.asarray(x, dtype=np.float64) for x in (Q, K, V, dO))
+    N, d = Q.shape
+    scale = 1.0 / np.sqrt(d)
+    k0, k1 = j * B, min(j * B + B, N)
+    q = np.asarray(queries, dtype=np.int64)
+    S = (Q[q] * scale) @ K[k0:k1].T
+    S = np.where(np.arange(k0, k1)[None, :] > q[:, None], -np.inf, S)
+    P = np.exp(S - np.asarray(L_q)[:, None])
+    Dq = (dO[q] * np.asarray(O_q)).sum(axis=1)
+    dS = P * (dO[q] @ V[k0:k1].T - Dq[:, None])
+    return dS.T @ (Q[q] * scale), P.T @ dO[q]

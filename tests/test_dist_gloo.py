@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2511_11571_b200.dist import gather_heads, shard_range
+from paper_2511_11571_b200.dist import gather_and_compare, gather_heads, shard_range
 
 
 def test_shard_range_partitions():
@@ -47,7 +47,13 @@ def _worker(rank, world, port, out_dir):
         outs.append(O)
     local = torch.tensor(np.stack(outs) if outs else np.zeros((0, N, d)))
     full = gather_heads(local, H)
+    # the verification helper bench.py uses: per-name bitwise flag + max diff
+    ref = None
     if rank == 0:
+        ref = {"O": torch.tensor(np.stack([orc.attention(Q[h], K[h], V[h], B, k)[0] for h in range(H)]))}
+    res = gather_and_compare({"O": local}, ref, H, torch.device("cpu"))
+    if rank == 0:
+        assert res["O"] == (True, 0.0), res
         torch.save(full, os.path.join(out_dir, "full.pt"))
     dist.barrier()
     dist.destroy_process_group()

@@ -43,7 +43,11 @@ def test_centroids_and_conv_vs_reference(name):
     if width:
         kern = mb.ConvKernel(g["W"])
         Kc = mb.key_conv_forward(K, kern)
-        assert_close(Kc, g["Kc"], "key_conv_forward", max_abs=3e-2, rel=5e-3)
+        # K' is returned from its bf16 kernel copy: round-to-nearest bf16 is
+        # within 2^-9 relative, so the bound is elementwise 2^-8 |K'| (2x
+        # margin) + 1e-6 for the fp32 conv arithmetic
+        err = np.abs(np.asarray(Kc, np.float64) - g["Kc"])
+        assert np.all(err <= 2.0 ** -8 * np.abs(g["Kc"]) + 1e-6), float((err - 2.0 ** -8 * np.abs(g["Kc"])).max())
         cents = mb.compute_centroids(K, B)  # raw-K centroids path
         ref_c, _ = orc.centroids(K, B)
         np.testing.assert_allclose(cents.centroids, ref_c, rtol=1e-5, atol=1e-6)
@@ -272,15 +276,23 @@ def test_moba_attn_conv_autograd():
         O, L = orc.forward(Qn[h], Kc, Vn[h], plan_o, B)
         _, rKc, _ = orc.backward(Qn[h], Kc, Vn[h], O, dOn[h], L, plan_o, B)
         dW = dW + orc.key_conv_backward(Kn[h], Wn, rKc)[1]
-    assert_close(w.grad.cpu().numpy(), dW, "conv dW", max_abs=5e-1, rel=1e-2)
+    # dW sums H x N terms g * K, so |dW| grows with H*N while every term
+    # carries the bf16-level error of dK' from the attention backward: the
+    # 2e-2 contract is applied relative to the largest entry
+    assert_close(w.grad.cpu().numpy(), dW, "conv dW", max_abs=2e-2 * max(1.0, float(np.abs(dW).max())))
 
 
 def test_key_conv_backward_vs_reference():
     for name in ("conv3_n512_b64", "conv5_n300_b32"):
         g = load(name)
         dK, dW = mb.key_conv_backward(f64(g["K"]), mb.ConvKernel(g["W"]), f64(g["dO"]))
-        assert_close(dK, g["conv_dK"], f"{name} conv dK", max_abs=3e-2, rel=5e-3)
-        assert_close(dW, g["conv_dW"], f"{name} conv dW", max_abs=5e-2, rel=1e-2)
+        # dK comes back from its bf16 kernel copy: elementwise 2^-8 |dK|
+        # (round-to-nearest bf16 is within 2^-9) + 1e-5 for the fp32 math;
+        # dW is fp32: the 2e-2 contract relative to its largest entry (a sum
+        # over N tokens)
+        err = np.abs(np.asarray(dK, np.float64) - g["conv_dK"])
+        assert np.all(err <= 2.0 ** -8 * np.abs(g["conv_dK"]) + 1e-5), name
+        assert_close(dW, g["conv_dW"], f"{name} conv dW", max_abs=2e-2 * max(1.0, float(np.abs(g["conv_dW"]).max())))
 
 
 @pytest.mark.slow
@@ -328,7 +340,8 @@ def _select_rows(Q, c, B, k, rows):
 @pytest.mark.parametrize("name", golden_names())
 def test_routing_tensor_core_mode_vs_reference(name):
     """Perf routing mode (bf16x3 centroid split on tcgen05): same selections as
-    the reference up to score near-ties (tolerance 1e-5 on the f64 score gap)."""
+    the reference up to score near-ties (the 1e-6 contract on the f64 score
+    gap)."""
     g = load(name)
     if int(g["d"]) > 128:
         pytest.skip("d > 128")
@@ -341,7 +354,7 @@ def test_routing_tensor_core_mode_vs_reference(name):
     w = pad(torch.tensor(g["W"], dtype=torch.float32).cuda()) if width else None
     cent, _ = _device.centroids(kt, B, w)
     plan = _device.route(qt, cent, B, k, mode=1)
-    bad, ndiff = unexcused_routing_rows(f64(g["Q"]), g["centroids"], plan.topk_indices, g["topk"], B, k, tol=1e-5)
+    bad, ndiff = unexcused_routing_rows(f64(g["Q"]), g["centroids"], plan.topk_indices, g["topk"], B, k)
     assert not bad, f"{len(bad)} rows differ beyond ties (of {ndiff}): {bad[:10]}"
     orc.validate_plan(orc.OraclePlan(plan.topk_indices, plan.counts, plan.offsets, plan.flat_queries),
                       int(g["N"]), B)
@@ -357,7 +370,7 @@ def test_routing_tensor_core_mode_c2_scale():
     Qn, Kn = q.double().cpu().numpy(), kk.double().cpu().numpy()
     for h in range(H):
         c, _ = orc.centroids(Kn[h], B)
-        bad, nd = unexcused_routing_rows(Qn[h], c, p_tc.topk_indices[h], p_fp.topk_indices[h], B, k, tol=1e-5)
+        bad, nd = unexcused_routing_rows(Qn[h], c, p_tc.topk_indices[h], p_fp.topk_indices[h], B, k)
         assert not bad, (h, bad[:5], nd)
 
 
@@ -576,3 +589,73 @@ def test_randomized_sweep_vs_oracle(N, B, k, d, hkv, G, conv, det):
     # bf16 once at the larger magnitude): the absolute tolerance scales with G
     assert_close(kg.grad.double().cpu().numpy(), dK, "dK", max_abs=2e-2 * G)
     assert_close(vg.grad.double().cpu().numpy(), dV, "dV", max_abs=2e-2 * G)
+
+
+def test_plan_with_disagreeing_layouts_rejected():
+    """A plan whose topk_indices name a (query, block) pair that flat_queries
+    does not list — with every count, offset and total still consistent —
+    is a PlanValidationError (src/core.py:254-296 checks both layouts)."""
+    rng = np.random.default_rng(13)
+    N, d, B, k = 512, 16, 32, 3
+    Q, K, V = (rng.standard_normal((N, d)) for _ in range(3))
+    cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    plan = mb.build_plan(Q, K, cfg)
+    idx = plan.topk_indices.copy()
+    i = N - 1
+    row = idx[i]
+    unused = [j for j in range(i // B) if j not in set(row.tolist())]
+    # move one routed block of query i to a block it did not pick: the row
+    # stays unique and causal, the totals are unchanged, flat still lists
+    # the old block
+    row[0] = unused[0]
+    idx[i] = np.sort(row)
+    plan.topk_indices = idx
+    with pytest.raises(mb.PlanValidationError):
+        mb.validate_plan(plan, N, cfg)
+    with pytest.raises(mb.PlanValidationError):
+        mb.moba_forward(Q, K, V, plan, cfg)
+
+
+def test_generic_f64_inputs_route_unrounded():
+    """numpy f64 inputs that are NOT bf16-representable: centroids and fp32
+    routing use the unrounded values, so the plan matches the f64 oracle up
+    to 1e-6 ties (rounding Q / K to bf16 first would move selections by
+    ~1e-2 score gaps); O / LSE / dQ / dK / dV stay within the 2e-2 contract."""
+    rng = np.random.default_rng(14)
+    N, d, B, k = 4096, 64, 64, 6
+    Q, K, V, dO = (rng.standard_normal((N, d)) for _ in range(4))
+    cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    res, plan = mb.moba_attention(Q, K, V, cfg)
+    c, _ = orc.centroids(K, B)
+    ref = orc.select_topk(Q, c, B, k)
+    bad, nd = unexcused_routing_rows(Q, c, plan.topk_indices, ref, B, k)
+    assert not bad, (len(bad), nd, bad[:5])
+    cents = mb.compute_centroids(K, B)
+    np.testing.assert_allclose(cents.centroids, c, rtol=1e-6, atol=1e-7)
+    op = orc.OraclePlan(plan.topk_indices, plan.counts, plan.offsets, plan.flat_queries)
+    O, L = orc.forward(Q, K, V, op, B)
+    assert_close(res.output, O, "O")
+    assert_close(res.logsumexp, L, "LSE")
+    dQ, dK, dV = mb.moba_backward(Q, K, V, res.output, dO, res.logsumexp, plan, cfg)
+    rQ, rK, rV = orc.backward(Q, K, V, O, dO, L, op, B)
+    assert_close(dQ, rQ, "dQ")
+    assert_close(dK, rK, "dK")
+    assert_close(dV, rV, "dV")
+
+
+def test_head_view_of_stale_plan_rebuilds_row_pos():
+    """RoutingPlan.head() of a plan whose fields were reassigned does not
+    inherit the stale (query, slot) -> flat position map."""
+    gen = torch.Generator(device="cuda").manual_seed(15)
+    H, N, d, B, k = 2, 1024, 64, 128, 3
+    q, kk, v = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(3))
+    cfg = mb.MobaConfig(block_size_B=B, top_k=k, head_dim_d=d)
+    plan = mb.build_plan(q, kk, cfg)
+    other = mb.build_plan(torch.flip(q, dims=[0]), kk, cfg)
+    plan.topk_indices = other.topk_indices
+    plan.counts, plan.offsets, plan.flat_queries = other.counts, other.offsets, other.flat_queries
+    h1 = plan.head(1)
+    assert h1.row_pos is None
+    res = mb.moba_forward(q[1:], kk[1:], v[1:], h1, cfg)
+    ref = mb.moba_forward(q[1:], kk[1:], v[1:], other.head(1), cfg)
+    assert torch.equal(res.output, ref.output)

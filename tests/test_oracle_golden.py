@@ -117,3 +117,27 @@ def test_flop_ratio_gate():
     r = orc.visible_pairs(8192, 128, 8) / (8192 * 8192)
     assert 0.115 <= r <= 0.135
     assert abs(r - 0.12408) < 1e-4
+
+
+@pytest.mark.parametrize("name", ["ragged_n500_b64", "conv3_n512_b64"])
+def test_row_and_block_restrictions_match_whole_head_oracle(name):
+    """forward_rows / backward_rows_dq / backward_block (used for sampled
+    checks at 512K) equal the whole-head oracle on a pinned fixture."""
+    g = load(name)
+    B = int(g["B"])
+    Q, V, dO = (f64(g[x]) for x in ("Q", "V", "dO"))
+    K = f64(g["Kc"]) if int(g["width"]) else f64(g["K"])
+    plan = orc.OraclePlan(g["topk"], g["counts"], g["offsets"], g["flat"])
+    O, L = orc.forward(Q, K, V, plan, B)
+    dQ, dK, dV = orc.backward(Q, K, V, O, dO, L, plan, B)
+    rows = np.arange(0, Q.shape[0], 7)
+    Or, Lr = orc.forward_rows(Q, K, V, rows, g["topk"][rows], B)
+    np.testing.assert_allclose(Or, O[rows], atol=1e-12)
+    np.testing.assert_allclose(Lr, L[rows], atol=1e-12)
+    dq = orc.backward_rows_dq(Q, K, V, O[rows], dO, L[rows], rows, g["topk"][rows], B)
+    np.testing.assert_allclose(dq, dQ[rows], atol=1e-12)
+    for j in (0, len(g["counts"]) - 1):
+        q = orc._block_slice(plan, j)
+        dk, dv = orc.backward_block(Q, K, V, dO, j, q, O[q], L[q], B)
+        np.testing.assert_allclose(dk, dK[j * B: j * B + len(dk)], atol=1e-12)
+        np.testing.assert_allclose(dv, dV[j * B: j * B + len(dv)], atol=1e-12)
