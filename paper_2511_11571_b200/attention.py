@@ -26,6 +26,7 @@ from . import _device
 from ._convert import from_heads, routing_heads, to_heads, to_weights
 from .core import (ConfigError, MobaConfig, OpCounters, PlanValidationError, RoutingPlan, ShapeError,
                    resolve_threads)
+from .counters import add_backward_counters, add_forward_counters, add_plan_counters
 from .router import ROUTE_MODES, build_plan
 
 
@@ -68,7 +69,7 @@ def moba_forward(Q, K, V, plan: RoutingPlan, cfg: MobaConfig,
     plan = _prepare_plan(plan, info, cfg, q.shape[0])
     out, lse = _device.fwd(q, k, v, plan, _device.softmax_scale(info.d))
     if counters is not None:
-        counters.attn_flops += 2 * info.d * _device.visible_pairs(plan)
+        add_forward_counters(counters, plan, info.d, cfg, _device.visible_pairs(plan))
     return AttentionOutput(from_heads(out, info), from_heads(lse, info, channels=False))
 
 
@@ -102,7 +103,7 @@ def moba_backward(Q, K, V, O, dO, lse, plan: RoutingPlan, cfg: MobaConfig,
     dq, dk, dv = _device.bwd(q, k, v, o, do, lse_t, plan, _device.softmax_scale(info.d),
                              deterministic=(schedule == "deterministic"))
     if counters is not None:
-        counters.attn_flops += 5 * info.d * _device.visible_pairs(plan)
+        add_backward_counters(counters, plan, info.d, cfg, _device.visible_pairs(plan))
     return from_heads(dq, info), from_heads(dk, info), from_heads(dv, info)
 
 
@@ -132,10 +133,9 @@ def moba_attention(Q, K, V, cfg: MobaConfig, counters: OpCounters | None = None,
     q32 = routing_heads(Q, "Q", device=q.device) if mode == "fp32" else None
     plan = _device.route(q if q32 is None else q32, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])
     out, lse = _device.fwd(q, k, v, plan, _device.softmax_scale(info.d))
-    if counters is not None:
-        H = q.shape[0]
-        counters.score_flops += H * _device.scored_candidates(info.n_tokens, cfg.block_size_B) * info.d
-        counters.attn_flops += 2 * info.d * _device.visible_pairs(plan)
+    if counters is not None:    # build_plan + moba_forward (src/attention.py:312-313)
+        add_plan_counters(counters, q.shape[0], info.n_tokens, info.d, cfg.block_size_B, cfg.phys_tile_Br)
+        add_forward_counters(counters, plan, info.d, cfg, _device.visible_pairs(plan))
     return AttentionOutput(from_heads(out, info), from_heads(lse, info, channels=False)), plan
 
 

@@ -89,11 +89,11 @@ class MobaConfig:
 class OpCounters:
     """Operation counters (src/core.py:193-226).
 
-    On the GPU path the counters are filled from the plan with the
-    reference's closed forms: attn_flops += 2*d per visible (query, key) pair
-    in the forward (src/attention.py:135) and 5*d in the backward
-    (src/attention.py:228); score_flops += d per scored (query, past block)
-    candidate (src/router.py:87).
+    On the GPU path the counters are filled from the plan in closed form
+    with the reference's tile knobs and classification rules
+    (paper_2511_11571_b200/counters.py): the same four numbers the
+    reference's tile walk produces (checked against reference-generated
+    values, tests/golden/counters.npz).
     """
 
     score_flops: int = 0

@@ -13,6 +13,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
+from .counters import add_plan_counters
 from ._convert import routing_heads, to_heads
 from .core import MobaConfig, OpCounters, PlanValidationError, RoutingPlan, ShapeError
 
@@ -50,8 +51,8 @@ def compute_centroids(K, B: int, counters: OpCounters | None = None) -> Centroid
     k, info = to_heads(K, "K")
     k32 = routing_heads(K, "K", device=k.device)
     cent, _ = _device.centroids(k if k32 is None else k32, B)
-    if counters is not None:
-        counters.bulk_elems += info.n_tokens * info.d + cent.shape[1] * info.d
+    if counters is not None:    # src/router.py:44-45
+        counters.bulk_elems += k.shape[0] * (info.n_tokens * info.d + cent.shape[1] * info.d)
     view = cent[..., : info.d]
     if info.kind == "numpy":
         view = view.reshape(*info.lead, cent.shape[1], info.d).cpu().numpy().astype(info.np_dtype)
@@ -71,8 +72,11 @@ def _route(Q, cents: CentroidMatrix, cfg: MobaConfig, counters, mode: str) -> tu
         raise ShapeError(f"centroid layout {tuple(cent.shape)} does not match Q {tuple(q.shape)}")
     q32 = routing_heads(Q, "Q", device=q.device) if mode == "fp32" else None
     plan = _device.route(q if q32 is None else q32, cent, cfg.block_size_B, cfg.top_k, ROUTE_MODES[mode])
-    if counters is not None:
-        counters.score_flops += q.shape[0] * _device.scored_candidates(info.n_tokens, cfg.block_size_B) * info.d
+    if counters is not None:    # select_topk only (src/router.py:85-88); the centroids were counted above
+        c = type(counters)()
+        add_plan_counters(c, q.shape[0], info.n_tokens, info.d, cfg.block_size_B, cfg.phys_tile_Br)
+        counters.score_flops += c.score_flops
+        counters.bulk_elems += c.bulk_elems - q.shape[0] * (info.n_tokens * info.d + cent.shape[1] * info.d)
     return plan, info
 
 
