@@ -40,6 +40,7 @@ class MobaLMConfig:
     conv_width: int = 0          # 0, 3 (kconv3) or 5 (kconv5) on the MoBA layers
     rope_base: float = 10000.0
     route_mode: str = "tc"
+    swa_impl: str = "flash"      # "flash" (FA2 windowed kernel) or "torch" (masked SDPA; tests, fp32 models)
 
 
 def _rope(x: torch.Tensor, base: float) -> torch.Tensor:
@@ -57,6 +58,7 @@ class Attention(nn.Module):
     def __init__(self, cfg: MobaLMConfig, moba: bool):
         super().__init__()
         self.cfg, self.moba = cfg, moba
+        self.moba_fn = moba_attn     # the MoBA operator (a test may swap in a reference implementation)
         inner = cfg.heads * cfg.head_dim
         self.qkv = nn.Linear(cfg.hidden, 3 * inner, bias=False)
         self.out = nn.Linear(inner, cfg.hidden, bias=False)
@@ -71,13 +73,20 @@ class Attention(nn.Module):
         q, k, v = self.qkv(x).view(b, N, 3, c.heads, c.head_dim).unbind(2)
         if self.moba:
             # MoBA layer: no positional encoding; [b, h, N, d] for the kernels
-            o = moba_attn(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), c.block_size, c.top_k,
-                          conv_weight=self.conv, mode=c.route_mode)
-            o = o.transpose(1, 2)
-        else:
+            # (bf16 operands; the output returns to the model's dtype)
+            o = self.moba_fn(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), c.block_size, c.top_k,
+                             conv_weight=self.conv, mode=c.route_mode)
+            o = o.transpose(1, 2).to(x.dtype)
+        elif c.swa_impl == "flash":
             from flash_attn import flash_attn_func
             q, k = _rope(q, c.rope_base), _rope(k, c.rope_base)
             o = flash_attn_func(q, k, v, causal=True, window_size=(c.swa_window - 1, 0))
+        else:
+            q, k = _rope(q, c.rope_base), _rope(k, c.rope_base)
+            i = torch.arange(N, device=x.device)
+            keep = (i[None, :] <= i[:, None]) & (i[:, None] - i[None, :] < c.swa_window)
+            o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2),
+                                               attn_mask=keep).transpose(1, 2)
         return self.out(o.reshape(b, N, c.heads * c.head_dim))
 
 

@@ -73,14 +73,31 @@ def test_report_matches_reference_schema():
         RunReport("x", {}, {"bad": float("nan")}).to_json()
 
 
-def test_cli_parser_and_config_merge(tmp_path):
+def test_cli_settings_layers(tmp_path):
+    """defaults < --config JSON object < explicit flags; unknown config keys
+    and missing required options are ConfigErrors (src/cli.py:54-68)."""
     from paper_2511_11571_b200 import cli
-    args = cli.build_parser().parse_args(["attend", "--q", "a", "--block", "64"])
-    cfg = tmp_path / "c.json"
-    cfg.write_text(json.dumps({"topk": 3, "block": 32}))
-    r = cli._resolve({"q": None, "block": 128, "topk": 8}, str(cfg), args)
-    assert r == {"q": "a", "block": 64, "topk": 3}          # flags override the file
-    cfg.write_text(json.dumps({"nope": 1}))
     from paper_2511_11571_b200.core import ConfigError
+    cfg = tmp_path / "c.json"
+    cfg.write_text(json.dumps({"topk": 3, "block": 32, "k": "kk", "v": "vv", "out": "o"}))
+    args = cli.build_parser().parse_args(["attend", "--q", "a", "--block", "64", "--config", str(cfg)])
+    s = cli.settings(cli.ATTEND, args)
+    assert (s["q"], s["block"], s["topk"], s["conv"], s["mode"]) == ("a", 64, 3, 0, "fp32")   # flag > file > default
+    cfg.write_text(json.dumps({"nope": 1}))
     with pytest.raises(ConfigError):
-        cli._resolve({"q": None}, str(cfg), args)
+        cli.settings(cli.ATTEND, args)
+    args = cli.build_parser().parse_args(["attend", "--q", "a"])
+    with pytest.raises(ConfigError):
+        cli.settings(cli.ATTEND, args)            # --k / --v / --out missing
+    b = cli.settings(cli.BENCH, cli.build_parser().parse_args(["bench", "--n", "256,512"]))
+    assert b["n"] == "256,512" and b["block"] == 128 and b["dim"] == 64
+
+
+def test_cli_errors_exit_2(tmp_path, capsys):
+    from paper_2511_11571_b200 import cli
+    rc = cli.main(["attend", "--q", "a"])
+    assert rc == 2
+    err = json.loads(capsys.readouterr().err)
+    assert err["error"] == "ConfigError"
+    rc = cli.main(["bench", "--n", "64", "--block", "128"])     # N shorter than the block
+    assert rc == 2
