@@ -1,6 +1,7 @@
 // Stages 2+3: tiled top-k routing and the key-block-major varlen plan.
 //
-//   select_topk  (src/router.py:49-120)   -> route_topk_fp32_kernel
+//   select_topk  (src/router.py:49-120)   -> route_topk_fp32_kernel (parity mode),
+//                                            route_tc_kernel (route_tc.cu, tensor cores)
 //   build_varlen (src/router.py:123-154)  -> varlen_count / varlen_scan /
 //                                            varlen_scatter kernels
 //   validate_plan (src/core.py:254-296)   -> validate_* kernels
@@ -206,246 +207,7 @@ route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent,
 }
 
 
-// ---------------------------------------------------------------- tensor-core routing
-// Perf mode (MOBA_ROUTE_TC). The fp32 centroid is split into three bf16 terms
-// c = c1 + c2 + c3 (24 mantissa bits); queries are bf16 already, so every
-// product q*ci is exact in fp32 and S = Q C1^T + Q C2^T + Q C3^T accumulates
-// in fp32 on tcgen05 (TMEM). Scores agree with the FFMA path to fp32 rounding
-// (ties within ~1e-6 may resolve differently, as documented).
-__global__ void centroid_split_kernel(const float* __restrict__ cent, int64_t total, __nv_bfloat16* __restrict__ split) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= total) return;
-    const float c = cent[e];
-    const __nv_bfloat16 c1 = __float2bfloat16(c);
-    const float r1 = c - __bfloat162float(c1);
-    const __nv_bfloat16 c2 = __float2bfloat16(r1);
-    const __nv_bfloat16 c3 = __float2bfloat16(r1 - __bfloat162float(c2));
-    split[e] = c1;
-    split[total + e] = c2;
-    split[2 * total + e] = c3;
-}
-
-constexpr int kRtM = 128;   // queries per CTA (TMEM lanes)
-constexpr int kRtN = 64;    // centroids per chunk (MMA N)
-
-// ---------------------------------------------------------------- tensor-core routing, 2 threads per query
-// Scores S = Q (C1 + C2 + C3)^T on tcgen05 (the bf16 hi/mid/lo split of the
-// fp32 centroids), the same selection order as route_topk_fp32_kernel; 8 warps per
-// CTA: the two warps of a TMEM lane quadrant split each 64-centroid chunk
-// (columns 0-31 / 32-63), each keeps its own running top-k of the query,
-// and the two lists (disjoint block sets, both ordered by score desc /
-// index asc) are merged at the end. Candidates are compacted 16 at a time
-// (per-lane smem lists of 16), so two CTAs fit on an SM.
-constexpr int kRt2Threads = 256;
-constexpr int kRt2Buf = 16;
-
-template <int KMAX>
-MOBA_DEV void select_chunk16(const float* sv, int j0, int lim, float (&ts)[KMAX], int (&ti)[KMAX], float* buf_s,
-                             int* buf_i) {
-    const float thr = ts[KMAX - 1];
-    int cnt = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        if (i < lim && sv[i] > thr) {
-            buf_s[cnt * 32] = sv[i];
-            buf_i[cnt * 32] = j0 + i;
-            ++cnt;
-        }
-    }
-    const int iters = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
-    for (int t = 0; t < iters; ++t) {
-        const float sc = buf_s[t * 32];
-        const int ix = buf_i[t * 32];
-        topk_insert_tail<KMAX>(ts, ti, (t < cnt && sc > ts[KMAX - 1]) ? sc : -INFINITY, ix);
-    }
-}
-
-template <int D, int KMAX>
-__global__ void __launch_bounds__(kRt2Threads)
-route_topk_tc2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c, int64_t N,
-                      int B, int top_k, int64_t split_rows, int kv_group, int c_bufs, int32_t* __restrict__ topk) {
-    using namespace sm100;
-    constexpr int SL = D / 64;
-    constexpr uint32_t q_bytes = kRtM * D * 2;
-    constexpr uint32_t c_bytes = kRtN * D * 2;            // one split term of a chunk
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* q_s = smem;
-    uint8_t* c_s = q_s + q_bytes;                         // [2 buffers][3 terms][SL][64][128B]
-    // c_bufs = 1 when every CTA has a single 64-centroid chunk (N <= 64 B):
-    // no second C buffer, smaller footprint, three CTAs per SM
-    uint64_t* bars = reinterpret_cast<uint64_t*>(c_s + c_bufs * 3 * c_bytes);   // tma[2], mma[2]
-    uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + 4);
-    float* sel_s = reinterpret_cast<float*>(tmem_ptr + 4);                   // [8 warps][16][32]
-    int* sel_i = reinterpret_cast<int*>(sel_s + 8 * kRt2Buf * 32);          // [8 warps][16][32]
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int quad = warp & 3, half = warp >> 2;
-    const int64_t h = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * kRtM;
-    const int n_blocks = (int)((N + B - 1) / B);
-    const int width = top_k + 1;
-    const int64_t last_i = min64(r0 + kRtM, N) - 1;
-    const int max_own = (int)(last_i / B);
-    const int n_chunks = (max_own + kRtN - 1) / kRtN;
-
-    if (warp == 0) tmem_alloc(tmem_ptr, 2 * kRtN);
-    if (tid == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_ptr;
-    const uint32_t idesc = idesc_bf16(kRtM, kRtN, false, false);
-
-    auto load_chunk = [&](int c, int buf) {   // thread 0
-        mbar_expect_tx(&bars[buf], 3 * c_bytes + (c == 0 ? q_bytes : 0));
-        if (c == 0) {
-#pragma unroll
-            for (int sl = 0; sl < SL; ++sl)
-                tma_load_2d(smem_u32(q_s) + sl * kRtM * 128, &tm_q, sl * 64, (int)(h * N + r0), &bars[buf]);
-        }
-        const uint32_t cb = smem_u32(c_s) + (c_bufs == 2 ? buf : 0) * 3 * c_bytes;
-#pragma unroll
-        for (int term = 0; term < 3; ++term)
-#pragma unroll
-            for (int sl = 0; sl < SL; ++sl)
-                tma_load_2d(cb + term * c_bytes + sl * kRtN * 128, &tm_c, sl * 64,
-                            (int)(term * split_rows + (h / kv_group) * n_blocks + (int64_t)c * kRtN), &bars[buf]);
-    };
-    auto issue_mma = [&](int c) {             // thread 0
-        const int buf = c & 1;
-        mbar_wait(&bars[buf], (c >> 1) & 1);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(q_s), cb = smem_u32(c_s) + (c_bufs == 2 ? buf : 0) * 3 * c_bytes;
-        bool acc = false;
-#pragma unroll
-        for (int term = 0; term < 3; ++term)
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-                const int sl = kk >> 2, ke = (kk & 3) * 16;
-                umma_bf16(tmem + buf * kRtN, desc_kmajor(qa + sl * kRtM * 128, ke),
-                          desc_kmajor(cb + term * c_bytes + sl * kRtN * 128, ke), idesc, acc);
-                acc = true;
-            }
-        umma_commit(&bars[2 + buf]);
-    };
-
-    // c_bufs = 2: chunk c+2 is loaded while chunk c is selected and MMA(c+1)
-    // runs ahead. c_bufs = 1 (one centroid buffer, smaller footprint, one
-    // more CTA per SM): chunk c+1 is loaded while chunk c is selected and
-    // its MMA is issued at the top of the next iteration. TMA barrier and
-    // TMEM slot of chunk c are c & 1 either way.
-    if (tid == 0 && n_chunks > 0) {
-        load_chunk(0, 0);
-        if (c_bufs == 2 && n_chunks > 1) load_chunk(1, 1);
-        issue_mma(0);
-    }
-
-    const int row = 32 * quad + lane;
-    const int64_t my_i = r0 + row;
-    const int my_own = (int)(min64(my_i, N - 1) / B);
-    const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
-    float* bs = sel_s + warp * kRt2Buf * 32 + lane;
-    int* bi = sel_i + warp * kRt2Buf * 32 + lane;
-    float ts[KMAX];
-    int ti[KMAX];
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u) {
-        ts[u] = -INFINITY;
-        ti[u] = 0x7fffffff;
-    }
-    for (int c = 0; c < n_chunks; ++c) {
-        const int buf = c & 1;
-        if (c_bufs == 1 && c > 0 && tid == 0) issue_mma(c);
-        mbar_wait(&bars[2 + buf], (c >> 1) & 1);        // S(c) in TMEM, smem buffer free
-        tc_fence_after();
-        if (tid == 0) {
-            if (c_bufs == 2) {
-                if (c + 1 < n_chunks) issue_mma(c + 1);
-                if (c + 2 < n_chunks) load_chunk(c + 2, buf);
-            } else if (c + 1 < n_chunks) {
-                load_chunk(c + 1, (c + 1) & 1);
-            }
-        }
-        const int j0 = c * kRtN + 32 * half;
-        const int lim = (my_i < N) ? min(32, my_own - j0) : 0;   // strictly-past blocks only
-        if (!__all_sync(0xffffffffu, lim <= 0)) {
-            float sv[32];
-            tmem_ld32(tmem + buf * kRtN + 32 * half + lane_off, sv);
-            tmem_ld_wait();
-            select_chunk16<KMAX>(sv, j0, lim, ts, ti, bs, bi);
-            if (!__all_sync(0xffffffffu, lim <= 16)) select_chunk16<KMAX>(sv + 16, j0 + 16, lim - 16, ts, ti, bs, bi);
-        }
-        tc_fence_before();
-        __syncthreads();                                 // S buffer may be overwritten by MMA(c + 2)
-    }
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 2 * kRtN);
-    }
-    // merge the two halves' lists: half 1 publishes, half 0 merges and writes
-    float* ms = reinterpret_cast<float*>(q_s);                 // [KMAX][128] (Q and C buffers are free now)
-    int* mi = reinterpret_cast<int*>(q_s + KMAX * kRtM * 4);
-    if (half == 1) {
-#pragma unroll
-        for (int u = 0; u < KMAX; ++u) {
-            ms[u * kRtM + row] = ts[u];
-            mi[u * kRtM + row] = ti[u];
-        }
-    }
-    __syncthreads();
-    if (half == 1 || my_i >= N) return;
-    int res[KMAX];
-    {
-        int a = 0, b = 0;
-        float bsc = ms[row];
-        int bix = mi[row];
-#pragma unroll
-        for (int u = 0; u < KMAX; ++u) {
-            float asc = -INFINITY;
-            int aix = 0x7fffffff;
-#pragma unroll
-            for (int v = 0; v < KMAX; ++v)
-                if (v == a) { asc = ts[v]; aix = ti[v]; }
-            const bool take_a = (asc > bsc) || (asc == bsc && aix < bix);
-            res[u] = take_a ? aix : bix;
-            if (take_a) {
-                ++a;
-            } else {
-                ++b;
-                bsc = (b < KMAX) ? ms[b * kRtM + row] : -INFINITY;
-                bix = (b < KMAX) ? mi[b * kRtM + row] : 0x7fffffff;
-            }
-        }
-    }
-    // keep the first top_k, sort the block ids ascending, append the own block
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u)
-        if (u >= top_k) res[u] = 0x7fffffff;
-#pragma unroll
-    for (int p = 0; p < KMAX; ++p) {
-#pragma unroll
-        for (int u = (p & 1); u + 1 < KMAX; u += 2) {
-            int x = res[u], y = res[u + 1];
-            res[u] = min(x, y);
-            res[u + 1] = max(x, y);
-        }
-    }
-    int32_t* out = topk + (h * N + my_i) * width;
-    int nvalid = 0;
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u) {
-        if (res[u] != 0x7fffffff) {
-            out[u] = res[u];
-            ++nvalid;
-        }
-    }
-    out[nvalid] = my_own;
-    for (int s2 = nvalid + 1; s2 < width; ++s2) out[s2] = -1;
-}
+// tensor-core routing (with the exactness guard): route_tc.cu
 
 // ---------------------------------------------------------------- varlen
 // build_varlen as a stable counting sort over query chunks:
@@ -928,6 +690,11 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     return check_launch("varlen_scatter_kernel");
 }
 
+size_t route_tc_ws_bytes(int64_t bh, int64_t N, int B);
+template <int D, int KMAX>
+int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, int64_t N, int B, int top_k,
+                    int32_t* topk, void* ws, cudaStream_t s);
+
 template <int D, int KMAX>
 static int launch_route(const void* q, bool q_f32, const float* cent, int64_t bh, int64_t N, int B, int top_k,
                         int mode, int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
@@ -941,28 +708,7 @@ static int launch_route(const void* q, bool q_f32, const float* cent, int64_t bh
         kern<<<grid, kRouteThreads, fsmem, s>>>((const float*)q, cent, N, B, top_k, kv_group, topk);
         return check_launch("route_topk_fp32_kernel");
     }
-    if (mode == MOBA_ROUTE_TC) {
-        const int64_t n = ceil_div(N, B);
-        const int64_t bh_kv = bh / kv_group;
-        const int64_t total = bh_kv * n * D;
-        __nv_bfloat16* split = (__nv_bfloat16*)split_ws;
-        centroid_split_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(cent, total, split);
-        int st = check_launch("centroid_split_kernel");
-        if (st) return st;
-        CUtensorMap tm_q, tm_c;
-        if (!make_tmap_bf16(&tm_q, q, (uint64_t)(bh * N), D, kRtM) ||
-            !make_tmap_bf16(&tm_c, split, (uint64_t)(3 * bh_kv * n), D, kRtN))
-            return MOBA_ERR_CUDA;
-        static_assert(kRtM * 64 * 2 + 3 * kRtN * 64 * 2 >= 2 * 32 * kRtM * 4, "merge area fits in the Q + C buffers");
-        // one centroid buffer: 3 CTAs per SM instead of 2 (measured 64K
-        // route 0.99 -> 0.86 ms against two buffers)
-        const int c_bufs = 1;
-        const size_t smem = 1024 + (size_t)kRtM * D * 2 + c_bufs * 3 * (size_t)kRtN * D * 2 + 64 + 2 * 8 * kRt2Buf * 32 * 4;
-        auto kern = route_topk_tc2_kernel<D, KMAX>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, kRt2Threads, smem, s>>>(tm_q, tm_c, N, B, top_k, bh_kv * n, kv_group, c_bufs, topk);
-        return check_launch("route_topk_tc2_kernel");
-    }
+    if (mode == MOBA_ROUTE_TC) return launch_route_tc<D, KMAX>(q, cent, bh, kv_group, N, B, top_k, topk, split_ws, s);
     auto kern = route_topk_fp32_kernel<D, KMAX, __nv_bfloat16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk);
@@ -996,7 +742,7 @@ static size_t varlen_ws_bytes(int64_t bh, int64_t n_tokens, int block_size) {
 extern "C" size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int block_size, int top_k) {
     (void)top_k;
     if (block_size < 1 || n_tokens < 1) return 0;
-    return varlen_ws_bytes(bh, n_tokens, block_size) + 3 * (size_t)bh * ceil_div(n_tokens, block_size) * 128 * 2;
+    return varlen_ws_bytes(bh, n_tokens, block_size) + route_tc_ws_bytes(bh, n_tokens, block_size);
 }
 
 static int route_impl(const void* q, bool q_f32, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
