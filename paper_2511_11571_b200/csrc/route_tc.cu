@@ -3,38 +3,47 @@
 //
 // Scores S = Q (C_hi + C_lo)^T on tcgen05: the fp32 centroids are split into
 // two bf16 terms (|c - c_hi - c_lo| <= 2^-16 |c|), Q is bf16 (exact), fp32
-// accumulation in TMEM. A CTA owns a tile of 128 queries (TMEM lanes) and
-// streams 128-centroid chunks (MMA N = 128) through a double-buffered TMEM
-// accumulator; tiles are launched longest first (the last tiles of a head
-// see the most past blocks).
+// accumulation in TMEM.
 //
-// Warps (288 threads):
-//   0      TMA (Q tile once, centroid chunks through CS smem stages) and MMA
-//          issue, one elected lane
-//   1-8    selection: the two warps of a TMEM lane quadrant split each chunk
-//          (columns 0-63 / 64-127). Per 16 candidates a thread builds a
-//          bitmask of the scores above its running threshold (two
-//          instructions per candidate); only when some lane has a hit are
-//          the 16 scores staged in shared memory and inserted, in ascending
-//          block order, into a sorted list of LS = top_k + 2 (ties keep the
-//          lower block index first, src/router.py:95-98).
+// Persistent kernel, one CTA per SM. A work unit is T consecutive 128-query
+// tiles of one head (T = 3 at d = 64, 2 at d = 128); every 128-centroid chunk
+// is loaded once per unit (TMA, CS smem stages) and multiplied, as two
+// N = 64 sub-chunks, into each tile's own double-buffered TMEM columns, so the
+// centroid traffic is shared by T tiles. Units are dealt round robin in
+// longest-first order (the last tiles of a head see the most past blocks).
 //
-// Exactness: the list keeps the two best candidates beyond the top k, so the
-// tensor-core selection can be certified against the fp32 router
-// (route_topk_fp32_kernel, whose scores are the fp32 FFMA chain over d):
-//   eps(row) = kEps(D) * |q| * max_j |c_j| bounds |s_tc - s_fp32| for every
-//   candidate of the row (split error 2^-16, tensor-core accumulation and
-//   the FFMA chain, x2 margin);
-//   s_k - s_{k+1} > 2 eps  -> the tensor-core top k IS the fp32 top k;
-//   s_k - s_{k+2} > 2 eps  -> the fp32 top k lies inside the k + 2 listed
-//                             candidates: they are rescored with the fp32
-//                             FFMA chain and reselected exactly (in-kernel);
-//   otherwise               -> the row is queued and route_recheck_kernel
-//                             reselects it over all its candidates in fp32.
-// The output is therefore bitwise the fp32 router's (the parity mode) for
-// every row.
+// Warps (32 x (1 + 5T) threads):
+//   0        TMA loads of the centroid chunks through the stages
+//   1 .. T   MMA issue, one warp per tile (its Q tile load, then its score
+//            sub-chunks, warp-uniform with one elected lane): the tiles do
+//            not wait for each other, only for their own buffers
+//   T+1 ..   selection: 4 warps per tile (TMEM lane quadrant = warp % 4),
+//            one query row per thread over every chunk of the row.
+//
+// Selection keeps a sorted list of LS = top_k + 4 packed 32-bit keys per
+// row: the order-preserving bits of the tensor-core score with the low
+// `idx_bits` replaced by (2^idx_bits - 1 - j), so one unsigned compare
+// orders by (truncated score desc, block index asc) and inserting a key
+// costs two IMNMX per list slot. A 16-candidate sub-group is filtered with
+// one FSETP per candidate against the list's threshold; only when some lane
+// of the warp has a hit are the 16 scores staged (lane-private smem) and the
+// hits inserted, one per lane per round.
+//
+// Exactness (the output is bitwise the fp32 router's, route_topk_fp32_kernel,
+// whose scores are the fp32 FFMA chain over d): with
+//   E(row) = (kEps(D) + 2^(idx_bits - 22)) * |q| * max_j |c_j|
+// bounding |key score - fp32 score| (split error, tensor-core accumulation,
+// FFMA chain, key truncation; x2 margins) and s_u the key score of list
+// entry u,
+//   s_{k-1} - s_k    > 2E -> the listed top k IS the fp32 top k;
+//   s_{k-1} - s_{LS-1} > 2E -> the fp32 top k lies inside the LS listed
+//                            entries: the warp rescoring them with the fp32
+//                            chain (one lane per entry) and reselects;
+//   otherwise              -> the row is queued for route_recheck_kernel
+//                            (full fp32 reselection over all its candidates).
 #include "common.cuh"
 #include "sm100.cuh"
+#include <algorithm>
 
 namespace moba {
 namespace rtc {
@@ -42,20 +51,24 @@ namespace rtc {
 constexpr int kM = 128;            // queries per tile (TMEM lanes)
 constexpr int kN = 128;            // centroids per chunk (MMA N)
 constexpr int kSplits = 2;         // bf16 hi + lo terms of the fp32 centroids
-constexpr int kSelWarps = 8;
-constexpr int kThreads = 32 * (1 + kSelWarps);
-constexpr int kGrp = 16;           // candidates per filter group
-constexpr int kStgStride = kGrp + 4;   // floats per lane in the staging area (conflict-free STS.128)
+constexpr int kW = 64;             // score columns per TMEM buffer (MMA N of one sub-chunk)
 
 template <int D>
 struct Geo {
-    static constexpr int CS = (D == 64) ? 2 : 1;                      // centroid smem stages
-    static constexpr uint32_t kQ = kM * D * 2;
+    static constexpr int T = (D == 64) ? 3 : 2;          // query tiles per unit (16 / 11 warps)
+    static constexpr int NBUF = (D == 64) ? 2 : 4;       // TMEM score buffers per tile
+    static constexpr int CS = (D == 64) ? 3 : 2;         // centroid chunk smem stages
+    static constexpr int kSelWarps = 4 * T;
+    static constexpr int kSel0 = 1 + T;                  // first selection warp
+    static constexpr int kThreads = 32 * (kSel0 + kSelWarps);
+    static constexpr uint32_t kQ = kM * D * 2;           // one query tile
     static constexpr uint32_t kCterm = kN * D * 2;
-    static constexpr uint32_t kC = kSplits * kCterm;
-    static constexpr uint32_t kStg = kSelWarps * 32 * kStgStride * 4;
-    static constexpr uint32_t kBars = 128;
-    static constexpr uint32_t kSmem = 1024 + kQ + CS * kC + kStg + kBars;
+    static constexpr uint32_t kC = kSplits * kCterm;     // one chunk stage
+    static constexpr uint32_t kStgWarp = 32 * 128;       // 32 scores per lane (16-B chunks swizzled by lane)
+    static constexpr uint32_t kBars = 512;
+    static constexpr uint32_t kSmem = 1024 + T * kQ + CS * kC + kSelWarps * kStgWarp + kBars;
+    static_assert(T * NBUF * kW <= 512, "the score buffers fit TMEM");
+    static_assert(kSmem <= 232448, "shared memory");
     // |s_tc - s_fp32| <= kEps * |q| * max|c|, with
     //   split:       2^-16 (two bf16 terms)
     //   tc accum.:   2 * (kSplits * D / 16 + 1) * 2^-23 (per K=16 MMA step, truncating)
@@ -66,9 +79,47 @@ struct Geo {
 };
 
 struct Bars {
-    uint64_t c_full[2], c_empty[2], s_full[2], s_free[2];
+    uint64_t c_full[3], c_empty[3], q_full[4], q_empty[4], s_full[4][4], s_free[4][4];
     uint32_t tmem;
 };
+
+// order-preserving unsigned image of an fp32 score (and its inverse)
+MOBA_DEV uint32_t okey(float s) {
+    const uint32_t u = __float_as_uint(s);
+    return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
+MOBA_DEV float okey_decode(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k); }
+// truncated score of a list key (a lower bound of the score it was built
+// from); -inf for the empty key 0
+MOBA_DEV float key_score(uint32_t k, uint32_t imask) { return k == 0u ? -INFINITY : okey_decode(k & ~imask); }
+
+// sorted (descending) insertion of x: slot u becomes max(ts[u], min(ts[u-1], x))
+// (keep, take x, or shift down) — every slot reads the old list, so the
+// network is two IMNMX deep instead of a chain through the list; x = 0 is a
+// no-op
+template <int LS>
+MOBA_DEV void key_insert(uint32_t (&ts)[LS], uint32_t x) {
+    uint32_t nw[LS];
+    nw[0] = max(ts[0], x);
+#pragma unroll
+    for (int u = 1; u < LS; ++u) nw[u] = max(ts[u], min(ts[u - 1], x));
+#pragma unroll
+    for (int u = 0; u < LS; ++u) ts[u] = nw[u];
+}
+
+// sorted insertion of two keys x >= y (merge of a 2-list): slot u becomes the
+// (u+1)-th largest of the union, max(ts[u], min(ts[u-1], x), min(ts[u-2], y));
+// one VIMNMX3 and two IMNMX per slot, all reading the old list
+template <int LS>
+MOBA_DEV void key_insert2(uint32_t (&ts)[LS], uint32_t x, uint32_t y) {
+    uint32_t nw[LS];
+    nw[0] = max(ts[0], x);
+    if (LS > 1) nw[1] = max(max(ts[1], min(ts[0], x)), y);
+#pragma unroll
+    for (int u = 2; u < LS; ++u) nw[u] = max(max(ts[u], min(ts[u - 1], x)), min(ts[u - 2], y));
+#pragma unroll
+    for (int u = 0; u < LS; ++u) ts[u] = nw[u];
+}
 
 // candidate (s, j) with j larger than every listed index: after every entry
 // with score >= s (ties keep the lower index first)
@@ -86,29 +137,6 @@ MOBA_DEV void list_insert(float (&ts)[LS], int (&ti)[LS], float s, int j) {
     }
     ts[0] = ge[0] ? ts[0] : s;
     ti[0] = ge[0] ? ti[0] : j;
-}
-
-// exact fp32 score = the fp32 router's FFMA chain (dd = 0 .. D-1 from 0),
-// q row from the bf16 SW128 smem tile (row `row` of a 128-row tile)
-template <int D>
-MOBA_DEV float exact_score_smem(uint32_t sq, int row, const float* __restrict__ c) {
-    float acc = 0.f;
-#pragma unroll
-    for (int cg = 0; cg < D / 8; ++cg) {
-        const int sl = cg >> 3, ch = cg & 7;
-        const int4 raw = lds128i(sq + sl * 128 * 128 + row * 128 + ((ch ^ (row & 7)) << 4));
-        const uint32_t u4[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
-        const float4 v0 = __ldg(reinterpret_cast<const float4*>(c + cg * 8));
-        const float4 v1 = __ldg(reinterpret_cast<const float4*>(c + cg * 8) + 1);
-        const float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 f = unpack_bf16(u4[e]);
-            acc = fmaf(f.x, cv[2 * e], acc);
-            acc = fmaf(f.y, cv[2 * e + 1], acc);
-        }
-    }
-    return acc;
 }
 
 // the same chain with q in registers
@@ -151,40 +179,86 @@ MOBA_DEV void write_row(int32_t* out, int (&res)[KMAX], int top_k, int own, int 
     for (int s = nvalid + 1; s < width; ++s) out[s] = -1;
 }
 
+
+
+// the lane's next pending hit of the group: its staged score (lane-private
+// row at stg, 16-B chunks XOR-swizzled by sx4) and its key-index field; the
+// no-op key source (score unused, idx 0 with key 0) when none is left
+MOBA_DEV bool next_hit(uint32_t& m, uint32_t stg, uint32_t sx4, float& s, uint32_t& e) {
+    if (m == 0u) return false;
+    e = (uint32_t)__ffs(m) - 1u;
+    m &= m - 1u;
+    asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(s) : "r"(stg | ((e << 2) ^ sx4)));
+    return true;
+}
+
+// exact fp32 score from global memory (the fp32 router's chain)
+template <int D>
+MOBA_DEV float exact_score_g(const __nv_bfloat16* __restrict__ q, const float* __restrict__ c) {
+    float acc = 0.f;
+#pragma unroll
+    for (int dd = 0; dd < D; dd += 8) {
+        float x[8];
+        ld8f(q + dd, x);
+        const float4 v0 = __ldg(reinterpret_cast<const float4*>(c + dd));
+        const float4 v1 = __ldg(reinterpret_cast<const float4*>(c + dd) + 1);
+        const float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = fmaf(x[e], cv[e], acc);
+    }
+    return acc;
+}
+
 template <int D, int KMAX>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(Geo<D>::kThreads, 1)
 route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c,
                 const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, const float* __restrict__ cmax2,
-                int64_t N, int B, int top_k, int64_t split_rows, int kv_group, int n_tiles,
-                int32_t* __restrict__ topk, int* __restrict__ recheck) {
+                int64_t N, int B, int top_k, int64_t split_rows, int kv_group, int bh, int n_tiles, int n_groups,
+                int idx_bits, int32_t* __restrict__ topk, int* __restrict__ recheck) {
     using namespace sm100;
     using G = Geo<D>;
-    constexpr int LS = KMAX + 2;
+    constexpr int T = G::T, NBUF = G::NBUF, CS = G::CS;
+    constexpr int LS = (KMAX + 4 < 32) ? KMAX + 4 : 32;
     constexpr int SL = D / 64;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sq = smem_u32(smem);
-    const uint32_t sc = sq + G::kQ;
-    float* stg = reinterpret_cast<float*>(smem + G::kQ + G::CS * G::kC);
-    Bars* bars = reinterpret_cast<Bars*>(smem + G::kQ + G::CS * G::kC + G::kStg);
+    const uint32_t sc = sq + T * G::kQ;
+    const uint32_t sstg = sc + CS * G::kC;
+    Bars* bars = reinterpret_cast<Bars*>(smem + T * G::kQ + CS * G::kC + G::kSelWarps * G::kStgWarp);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t h = blockIdx.x;
-    const int tile = n_tiles - 1 - (int)blockIdx.y;          // longest tiles first
-    const int64_t r0 = (int64_t)tile * kM;
     const int n_blocks = (int)((N + B - 1) / B);
     const int width = top_k + 1;
-    const int max_own = (int)((min64(r0 + kM, N) - 1) / B);
-    const int n_chunks = (max_own + kN - 1) / kN;
-    const int64_t hk = h / kv_group;
+    const int total = bh * n_groups;
+    const int n_my = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // unit i of this CTA -> (head, tile group), longest first
+    auto unit_h = [&](int i) { return (int)(((int)blockIdx.x + i * (int)gridDim.x) % bh); };
+    auto unit_g = [&](int i) { return n_groups - 1 - ((int)blockIdx.x + i * (int)gridDim.x) / bh; };
+    // 64-centroid sub-chunks tile t needs: candidates j < own <= own of its last row
+    auto tile_nsub = [&](int t) -> int {
+        if (t >= n_tiles) return 0;
+        const int mo = (int)((min64((int64_t)(t + 1) * kM, N) - 1) / B);
+        return (mo + kW - 1) / kW;
+    };
+    auto unit_nch = [&](int i) {
+        const int t = min(unit_g(i) * T + T - 1, n_tiles - 1);
+        return (tile_nsub(t) + 1) / 2;
+    };
 
-    if (warp == 0) tmem_alloc(&bars->tmem, 2 * kN);
+    if (warp == 0) tmem_alloc(&bars->tmem, 512);
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < CS; ++i) {
             mbar_init(&bars->c_full[i], 1);
-            mbar_init(&bars->c_empty[i], 1);
-            mbar_init(&bars->s_full[i], 1);
-            mbar_init(&bars->s_free[i], kSelWarps);
+            mbar_init(&bars->c_empty[i], T);
+        }
+        for (int t = 0; t < T; ++t) {
+            mbar_init(&bars->q_full[t], 1);
+            mbar_init(&bars->q_empty[t], 1 + 4);
+            for (int b = 0; b < NBUF; ++b) {
+                mbar_init(&bars->s_full[t][b], 1);
+                mbar_init(&bars->s_free[t][b], 4);
+            }
         }
         fence_mbar_init();
     }
@@ -194,168 +268,123 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     const uint32_t tmem = bars->tmem;
 
     if (warp == 0) {
-        // ------------------------------------------------------------ TMA + MMA
-        if (n_chunks > 0) {
-            const uint32_t idesc = idesc_bf16(kM, kN, false, false);
-            auto load = [&](int c) {
-                const int st = c % G::CS;
-                const uint32_t dst = sc + st * G::kC;
+        // ------------------------------------------------------------ centroid loader
+        int gl = 0;
+        for (int i = 0; i < n_my; ++i) {
+            const int nch = unit_nch(i);
+            const int64_t hk = unit_h(i) / kv_group;
+            for (int c = 0; c < nch; ++c, ++gl) {
+                const int st = gl % CS;
+                if (gl >= CS) mbar_wait_sleep(&bars->c_empty[st], ((gl / CS) - 1) & 1);
                 if (lane == 0) {
-                    mbar_expect_tx(&bars->c_full[st], G::kC + (c == 0 ? G::kQ : 0));
-                    if (c == 0)
-#pragma unroll
-                        for (int sl = 0; sl < SL; ++sl)
-                            tma_load_2d(sq + sl * kM * 128, &tm_q, sl * 64, (int)(h * N + r0), &bars->c_full[st]);
+                    mbar_expect_tx(&bars->c_full[st], G::kC);
 #pragma unroll
                     for (int t = 0; t < kSplits; ++t)
 #pragma unroll
                         for (int sl = 0; sl < SL; ++sl)
-                            tma_load_2d(dst + t * G::kCterm + sl * kN * 128, &tm_c, sl * 64,
+                            tma_load_2d(sc + st * G::kC + t * G::kCterm + sl * kN * 128, &tm_c, sl * 64,
                                         (int)(t * split_rows + hk * n_blocks + (int64_t)c * kN), &bars->c_full[st]);
                 }
                 __syncwarp();
-            };
-            for (int c = 0; c < min(G::CS, n_chunks); ++c) load(c);
-            for (int c = 0; c < n_chunks; ++c) {
-                const int st = c % G::CS, slot = c & 1;
-                mbar_wait(&bars->c_full[st], (c / G::CS) & 1);
-                if (c >= 2) mbar_wait(&bars->s_free[slot], ((c >> 1) - 1) & 1);
-                tc_fence_after();
+            }
+        }
+    } else if (warp < G::kSel0) {
+        // ------------------------------------------------------------ MMA issuer of tile warp - 1
+        // (its own Q tile load, then S sub-chunks into the tile's buffers;
+        // a chunk stage is released once every tile's MMAs have read it)
+        const int tt = warp - 1;
+        const uint32_t idesc = idesc_bf16(kM, kW, false, false);
+        int gm = 0, qc = 0, scnt[NBUF];
+#pragma unroll
+        for (int b = 0; b < NBUF; ++b) scnt[b] = 0;
+        for (int i = 0; i < n_my; ++i) {
+            const int h = unit_h(i), t = unit_g(i) * T + tt;
+            const int nch = unit_nch(i);
+            const int nsub = tile_nsub(t);
+            if (nsub > 0) {
+                if (qc > 0) mbar_wait_sleep(&bars->q_empty[tt], (qc - 1) & 1);
+                if (lane == 0) {
+                    mbar_expect_tx(&bars->q_full[tt], G::kQ);
+#pragma unroll
+                    for (int sl = 0; sl < SL; ++sl)
+                        tma_load_2d(sq + tt * G::kQ + sl * kM * 128, &tm_q, sl * 64,
+                                    (int)((int64_t)h * N + (int64_t)t * kM), &bars->q_full[tt]);
+                }
+                __syncwarp();
+            }
+            for (int c = 0; c < nch; ++c) {
+                const int st = (gm + c) % CS;
+                mbar_wait_sleep(&bars->c_full[st], ((gm + c) / CS) & 1);
+                if (2 * c >= nsub) {
+                    if (lane == 0) mbar_arrive(&bars->c_empty[st]);
+                    __syncwarp();
+                    continue;
+                }
+                if (c == 0) mbar_wait_sleep(&bars->q_full[tt], qc & 1);
                 const uint32_t cb = sc + st * G::kC;
 #pragma unroll
-                for (int t = 0; t < kSplits; ++t)
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int sub = 2 * c + hf;
+                    if (sub >= nsub) continue;
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const int sl = kk >> 2, ke = (kk & 3) * 16;
-                        umma_bf16_w(tmem + slot * kN, desc_kmajor(sq + sl * kM * 128, ke),
-                                    desc_kmajor(cb + t * G::kCterm + sl * kN * 128, ke), idesc, t > 0 || kk > 0);
+                    for (int b = 0; b < NBUF; ++b) {
+                        if ((sub % NBUF) != b) continue;
+                        if (scnt[b] > 0) mbar_wait_sleep(&bars->s_free[tt][b], (scnt[b] - 1) & 1);
+                        tc_fence_after();
+                        const uint32_t dst = tmem + (uint32_t)((tt * NBUF + b) * kW);
+#pragma unroll
+                        for (int t2 = 0; t2 < kSplits; ++t2)
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const int sl = kk >> 2, ke = (kk & 3) * 16;
+                                umma_bf16_w(dst, desc_kmajor(sq + tt * G::kQ + sl * kM * 128, ke),
+                                            desc_kmajor(cb + t2 * G::kCterm + sl * kN * 128 + hf * kW * 128, ke),
+                                            idesc, t2 > 0 || kk > 0);
+                            }
+                        umma_commit_w(&bars->s_full[tt][b]);
+                        ++scnt[b];
                     }
-                umma_commit_w(&bars->s_full[slot]);
+                }
                 umma_commit_w(&bars->c_empty[st]);
-                if (c + G::CS < n_chunks) {
-                    mbar_wait(&bars->c_empty[st], (c / G::CS) & 1);   // MMA(c) has read the stage
-                    load(c + G::CS);
+                if (2 * c + 2 >= nsub) {
+                    umma_commit_w(&bars->q_empty[tt]);
+                    ++qc;
                 }
             }
+            gm += nch;
         }
     } else {
         // ------------------------------------------------------------ selection
-        const int sw = warp - 1;
-        const int quad = warp & 3, half = sw >> 2;
+        const int sw = warp - G::kSel0, tt = sw >> 2, quad = warp & 3;
         const int row = 32 * quad + lane;
-        const int64_t my_i = r0 + row;
-        const bool valid = my_i < N;
-        const int my_own = (int)(min64(my_i, N - 1) / B);
         const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
-        float* my_stg = stg + (sw * 32 + lane) * kStgStride;
-        float ts[LS];
-        int ti[LS];
+        const uint32_t stg = sstg + sw * G::kStgWarp + lane * 128;
+        const uint32_t sxor = (uint32_t)(lane & 7), sx4 = sxor << 4;
+        const uint32_t imask = (1u << idx_bits) - 1u;
+        const float gstep = ldexpf(1.f, idx_bits - 22);   // key grid step / 2^exponent (x2 margin)
+        int qcnt = 0, scnt[NBUF];
 #pragma unroll
-        for (int u = 0; u < LS; ++u) {
-            ts[u] = -INFINITY;
-            ti[u] = 0x7fffffff;
-        }
-        for (int c = 0; c < n_chunks; ++c) {
-            const int slot = c & 1;
-            const int j0 = c * kN + 64 * half;
-            const int lim = valid ? max(0, min(64, my_own - j0)) : 0;   // strictly-past blocks only
-            mbar_wait(&bars->s_full[slot], (c >> 1) & 1);
-            tc_fence_after();
-            float sv[64];
-            if (__any_sync(0xffffffffu, lim > 0)) {
-                tmem_ld32(tmem + slot * kN + 64 * half + lane_off, *reinterpret_cast<float(*)[32]>(&sv[0]));
-                tmem_ld32(tmem + slot * kN + 64 * half + 32 + lane_off, *reinterpret_cast<float(*)[32]>(&sv[32]));
-                tmem_ld_wait();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->s_free[slot]);
-            if (!__any_sync(0xffffffffu, lim > 0)) continue;
+        for (int b = 0; b < NBUF; ++b) scnt[b] = 0;
+        for (int i = 0; i < n_my; ++i) {
+            const int h = unit_h(i), t = unit_g(i) * T + tt;
+            if (t >= n_tiles) continue;
+            const int64_t hk = h / kv_group;
+            const int64_t r0 = (int64_t)t * kM;
+            const int64_t my_i = r0 + row;
+            const bool valid = my_i < N;
+            const int own = valid ? (int)(my_i / B) : 0;
+            const int nsub = tile_nsub(t);
+            uint32_t ts[LS];
 #pragma unroll
-            for (int g = 0; g < 64 / kGrp; ++g) {
-                const float thr = ts[LS - 1];
-                uint32_t m = 0;
-#pragma unroll
-                for (int i = 0; i < kGrp; ++i) m |= (sv[g * kGrp + i] > thr) ? (1u << i) : 0u;
-                const int rem = lim - g * kGrp;
-                m &= rem >= kGrp ? 0xffffu : (rem > 0 ? (1u << rem) - 1u : 0u);
-                if (!__any_sync(0xffffffffu, m != 0)) continue;
-                if (m != 0) {
-#pragma unroll
-                    for (int i = 0; i < kGrp; i += 4)
-                        *reinterpret_cast<float4*>(my_stg + i) =
-                            make_float4(sv[g * kGrp + i], sv[g * kGrp + i + 1], sv[g * kGrp + i + 2], sv[g * kGrp + i + 3]);
-                }
-                while (__any_sync(0xffffffffu, m != 0)) {
-                    float s = -INFINITY;
-                    int j = 0x7fffffff;
-                    if (m != 0) {
-                        const int b = __ffs(m) - 1;
-                        m &= m - 1;
-                        s = my_stg[b];
-                        j = j0 + g * kGrp + b;
-                    }
-                    list_insert<LS>(ts, ti, s > ts[LS - 1] ? s : -INFINITY, j);
-                }
-            }
-        }
-        // ---- merge the two halves' lists (the C stages are free now)
-        float* ms = reinterpret_cast<float*>(smem + G::kQ);            // [LS][128]
-        int* mi = reinterpret_cast<int*>(smem + G::kQ + LS * kM * 4);  // [LS][128]
-        if (half == 1) {
-#pragma unroll
-            for (int u = 0; u < LS; ++u) {
-                ms[u * kM + row] = ts[u];
-                mi[u * kM + row] = ti[u];
-            }
-        }
-        named_bar(1 + quad, 64);
-        if (half == 0 && valid) {
-            float rs[LS];
-            int ri[LS];
-            {
-                int a = 0, b = 0;
-                float bsc = ms[row];
-                int bix = mi[row];
-#pragma unroll
-                for (int u = 0; u < LS; ++u) {
-                    float asc = -INFINITY;
-                    int aix = 0x7fffffff;
-#pragma unroll
-                    for (int v = 0; v < LS; ++v)
-                        if (v == a) {
-                            asc = ts[v];
-                            aix = ti[v];
-                        }
-                    const bool take_a = better(asc, aix, bsc, bix);
-                    rs[u] = take_a ? asc : bsc;
-                    ri[u] = take_a ? aix : bix;
-                    if (take_a) {
-                        ++a;
-                    } else {
-                        ++b;
-                        bsc = (b < LS) ? ms[b * kM + row] : -INFINITY;
-                        bix = (b < LS) ? mi[b * kM + row] : 0x7fffffff;
-                    }
-                }
-            }
-            int res[KMAX];
-#pragma unroll
-            for (int u = 0; u < KMAX; ++u) res[u] = ri[u];
-            if (my_own > top_k) {
-                // ---- exactness guard
-                float sk = -INFINITY, sk1 = -INFINITY, sk2 = -INFINITY;
-#pragma unroll
-                for (int u = 0; u < LS; ++u) {
-                    if (u == top_k - 1) sk = rs[u];
-                    if (u == top_k) sk1 = rs[u];
-                    if (u == top_k + 1) sk2 = rs[u];
-                }
-                float qn = 0.f;
+            for (int u = 0; u < LS; ++u) ts[u] = 0u;
+            float qn = 0.f;
+            if (nsub > 0) {
+                mbar_wait(&bars->q_full[tt], qcnt & 1);
+                ++qcnt;
 #pragma unroll
                 for (int cg = 0; cg < D / 8; ++cg) {
                     const int sl = cg >> 3, ch = cg & 7;
-                    const int4 raw = lds128i(sq + sl * kM * 128 + row * 128 + ((ch ^ (row & 7)) << 4));
+                    const int4 raw = lds128i(sq + tt * G::kQ + sl * kM * 128 + row * 128 + ((ch ^ (row & 7)) << 4));
                     const uint32_t u4[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -363,50 +392,165 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                         qn = fmaf(f.x, f.x, fmaf(f.y, f.y, qn));
                     }
                 }
-                const float eps = G::kEps * sqrtf(qn) * sqrtf(__ldg(cmax2 + hk));
-                if (!(sk - sk1 > 2.f * eps)) {
-                    if (sk - sk2 > 2.f * eps) {
-                        // the fp32 top k lies among the k + 2 listed candidates:
-                        // rescore them with the fp32 chain and reselect exactly
-                        const float* Ch = cent + hk * (int64_t)n_blocks * D;
-                        float es[KMAX + 2];
-                        int ei[KMAX + 2];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->q_empty[tt]);
+                const int wown = __reduce_max_sync(0xffffffffu, own);
+                float thr = -INFINITY;
+                for (int sub = 0; sub < nsub; ++sub) {
+                    const int b = sub % NBUF;
 #pragma unroll
-                        for (int u = 0; u < KMAX + 2; ++u) {
-                            ei[u] = (u < top_k + 2) ? ri[u] : 0x7fffffff;
-                            es[u] = (ei[u] != 0x7fffffff) ? exact_score_smem<D>(sq, row, Ch + (int64_t)ei[u] * D) : -INFINITY;
+                    for (int bb = 0; bb < NBUF; ++bb)
+                        if (bb == b) {
+                            mbar_wait(&bars->s_full[tt][bb], scnt[bb] & 1);
+                            ++scnt[bb];
                         }
-                        // selection sort of the top_k by (score desc, index asc)
+                    tc_fence_after();
+                    const int ng = max(0, min(kW / 32, (wown - sub * kW + 31) / 32));
+                    const uint32_t scol = tmem + (uint32_t)((tt * NBUF + b) * kW) + lane_off;
+                    if (ng == 0) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&bars->s_free[tt][b]);
+                    }
+                    for (int g = 0; g < ng; ++g) {
+                        const int j0 = sub * kW + 32 * g;
+                        const int lim = max(0, min(32, own - j0));
+                        const uint32_t jb = imask - (uint32_t)j0;
+                        const bool warm = sub == 0 && g == 0 && __reduce_max_sync(0xffffffffu, lim) >= 12;
+                        uint32_t m = 0;
+                        // two 16-column halves keep the register peak low
 #pragma unroll
-                        for (int p = 0; p < KMAX; ++p) {
-#pragma unroll
-                            for (int u = p + 1; u < KMAX + 2; ++u) {
-                                if (better(es[u], ei[u], es[p], ei[p])) {
-                                    const float t = es[p];
-                                    es[p] = es[u];
-                                    es[u] = t;
-                                    const int ti2 = ei[p];
-                                    ei[p] = ei[u];
-                                    ei[u] = ti2;
-                                }
+                        for (int hh = 0; hh < 2; ++hh) {
+                            float sv[16];
+                            tmem_ld16(scol + 32 * g + 16 * hh, sv);
+                            tmem_ld_wait();
+                            if (g == ng - 1 && hh == 1) {
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&bars->s_free[tt][b]);
                             }
-                            res[p] = ei[p];
+                            if (warm) {
+                                // empty lists: insert the first 32 candidates unconditionally
+#pragma unroll
+                                for (int e = 0; e < 16; e += 2) {
+                                    const uint32_t k0 = 16 * hh + e < lim
+                                                            ? (okey(sv[e]) & ~imask) | (jb - (uint32_t)(16 * hh + e)) : 0u;
+                                    const uint32_t k1 = 16 * hh + e + 1 < lim
+                                                            ? (okey(sv[e + 1]) & ~imask) | (jb - (uint32_t)(16 * hh + e + 1)) : 0u;
+                                    key_insert2<LS>(ts, max(k0, k1), min(k0, k1));
+                                }
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 16; ++e) m |= (sv[e] >= thr) ? (1u << (16 * hh + e)) : 0u;
+#pragma unroll
+                                for (int e = 0; e < 16; e += 4)
+                                    sts128(stg + ((((uint32_t)(16 * hh + e) >> 2) ^ sxor) << 4),
+                                           make_uint4(__float_as_uint(sv[e]), __float_as_uint(sv[e + 1]),
+                                                      __float_as_uint(sv[e + 2]), __float_as_uint(sv[e + 3])));
+                            }
                         }
-                    } else {
-                        // two near-ties at the boundary: full fp32 reselection of the row
-                        const int slotq = atomicAdd(recheck, 1);
-                        recheck[1 + slotq] = (int)(h * N + my_i);
+                        m &= lim >= 32 ? 0xffffffffu : (1u << max(lim, 0)) - 1u;
+                        if (!warm && __any_sync(0xffffffffu, m != 0u)) {
+                            // two hits per lane per round (a 2-key merge), the
+                            // next round's scores loaded while this one merges
+                            float s0 = 0.f, s1 = 0.f;
+                            uint32_t e0 = 0u, e1 = 0u;
+                            bool v0 = next_hit(m, stg, sx4, s0, e0);
+                            bool v1 = next_hit(m, stg, sx4, s1, e1);
+                            do {
+                                float s2 = 0.f, s3 = 0.f;
+                                uint32_t e2 = 0u, e3 = 0u;
+                                const bool v2 = next_hit(m, stg, sx4, s2, e2);
+                                const bool v3 = next_hit(m, stg, sx4, s3, e3);
+                                const uint32_t k0 = v0 ? (okey(s0) & ~imask) | (jb - e0) : 0u;
+                                const uint32_t k1 = v1 ? (okey(s1) & ~imask) | (jb - e1) : 0u;
+                                key_insert2<LS>(ts, max(k0, k1), min(k0, k1));
+                                v0 = v2;
+                                v1 = v3;
+                                s0 = s2;
+                                s1 = s3;
+                                e0 = e2;
+                                e1 = e3;
+                            } while (__any_sync(0xffffffffu, v0));
+                        }
+                        thr = key_score(ts[LS - 1], imask);
                     }
                 }
             }
-            write_row<KMAX>(topk + (h * N + my_i) * width, res, top_k, my_own, width);
+            // ---------------------------------------------------------------- guard
+            int res[KMAX];
+#pragma unroll
+            for (int u = 0; u < KMAX; ++u)
+                res[u] = (u < top_k && ts[u] != 0u) ? (int)(imask - (ts[u] & imask)) : 0x7fffffff;
+            int status = 0;
+            if (valid && own > top_k) {
+                // entries k-1 and k by a select chain (an indexed read would
+                // send the whole list to local memory)
+                uint32_t kk0 = 0u, kk1 = 0u;
+#pragma unroll
+                for (int u = 0; u < LS; ++u) {
+                    uint32_t v;
+                    asm volatile("mov.b32 %0, %1;\n" : "=r"(v) : "r"(ts[u]));
+                    kk0 = (u == top_k - 1) ? v : kk0;
+                    kk1 = (u == top_k) ? v : kk1;
+                }
+                // s_tc of a listed entry lies in [key score, key score + grid step);
+                // every entry at or below position u has s_tc < upper(u)
+                auto upper = [&](uint32_t key) {
+                    const float v = key_score(key, imask);
+                    return key == 0u ? -INFINITY : v + __uint_as_float(__float_as_uint(v) & 0x7f800000u) * gstep;
+                };
+                const float lo = key_score(kk0, imask);
+                const float e2 = 2.f * G::kEps * sqrtf(qn) * sqrtf(__ldg(cmax2 + hk));
+                if (!(lo - upper(kk1) > e2)) status = (lo - upper(ts[LS - 1]) > e2) ? 1 : 2;
+            }
+            // rows whose fp32 top k lies inside the list: the warp rescores
+            // them one row at a time, lane u taking list entry u
+            uint32_t rm = __ballot_sync(0xffffffffu, status == 1);
+            while (rm != 0u) {
+                const int r = __ffs(rm) - 1;
+                rm &= rm - 1u;
+                int cand = -1;
+#pragma unroll
+                for (int u = 0; u < LS; ++u) {
+                    const uint32_t kv = __shfl_sync(0xffffffffu, ts[u], r);
+                    if (lane == u && kv != 0u) cand = (int)(imask - (kv & imask));
+                }
+                const int64_t qrow = (int64_t)h * N + r0 + 32 * quad + r;
+                float es = -INFINITY;
+                int ei = 0x7fffffff;
+                if (cand >= 0) {
+                    es = exact_score_g<D>(Q + qrow * D, cent + (hk * n_blocks + cand) * (int64_t)D);
+                    ei = cand;
+                }
+                int rank = 0;
+#pragma unroll
+                for (int src = 0; src < LS; ++src) {
+                    const float os = __shfl_sync(0xffffffffu, es, src);
+                    const int oi = __shfl_sync(0xffffffffu, ei, src);
+                    rank += better(os, oi, es, ei) ? 1 : 0;
+                }
+                uint32_t sel = __ballot_sync(0xffffffffu, cand >= 0 && rank < top_k);
+#pragma unroll
+                for (int p = 0; p < KMAX; ++p) {
+                    const int l = sel != 0u ? __ffs(sel) - 1 : 0;
+                    sel &= sel - 1u;
+                    const int v = __shfl_sync(0xffffffffu, ei, l);
+                    if (lane == r && p < top_k) res[p] = v;
+                }
+            }
+            if (status == 2) {
+                const int slot = atomicAdd(recheck, 1);
+                recheck[1 + slot] = (int)((int64_t)h * N + my_i);
+            }
+            if (valid) write_row<KMAX>(topk + ((int64_t)h * N + my_i) * width, res, top_k, own, width);
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, 2 * kN);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -528,10 +672,18 @@ int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, 
         !make_tmap_bf16(&tm_c, split, (uint64_t)(2 * rows), D, kN))
         return MOBA_ERR_CUDA;
     const int n_tiles = (int)ceil_div(N, kM);
+    const int n_groups = (int)ceil_div(n_tiles, Geo<D>::T);
+    const int64_t units = bh * n_groups;
+    if (units >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
+    int idx_bits = 1;
+    while ((1ll << idx_bits) < n) ++idx_bits;
+    if (idx_bits > 20) return MOBA_ERR_UNSUPPORTED;
     auto kern = route_tc_kernel<D, KMAX>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<D>::kSmem);
-    kern<<<dim3((unsigned)bh, (unsigned)n_tiles), kThreads, Geo<D>::kSmem, s>>>(
-        tm_q, tm_c, (const __nv_bfloat16*)q, cent, cmax2, N, B, top_k, rows, kv_group, n_tiles, topk, recheck);
+    const unsigned grid = (unsigned)std::min<int64_t>(units, kNumSMs);
+    kern<<<grid, Geo<D>::kThreads, Geo<D>::kSmem, s>>>(tm_q, tm_c, (const __nv_bfloat16*)q, cent, cmax2, N, B, top_k,
+                                                       rows, kv_group, (int)bh, n_tiles, n_groups, idx_bits, topk,
+                                                       recheck);
     st = check_launch("route_tc_kernel");
     if (st) return st;
     route_recheck_kernel<D, KMAX><<<kNumSMs * 2, 256, 0, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group,

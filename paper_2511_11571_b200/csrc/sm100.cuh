@@ -62,6 +62,30 @@ MOBA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Blocking wait for roles off the critical issue path (producers, MMA
+// issuers): try_wait with a suspend-time hint parks the warp until the phase
+// completes (or ~the hint elapses) instead of re-polling, leaving the issue
+// slots to the compute warps. Same watchdog as mbar_wait.
+MOBA_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
+        : "memory");
+    return ok != 0;
+}
+MOBA_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    if (mbar_try_wait_sleep(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait_sleep(bar, parity)) {
+        __nanosleep(500);
+        if (clock64() - t0 > 20000000000ll) asm volatile("trap;");
+    }
+}
+
 // arrive on `bar` when all cp.async issued so far by this thread complete
 // (no pending-count increment: the barrier's expected count includes it)
 MOBA_DEV void cpasync_arrive_noinc(uint64_t* bar) {
