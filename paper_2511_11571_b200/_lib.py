@@ -13,7 +13,7 @@ import os
 from .core import ConfigError, MobaError, PlanValidationError, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoba_b200.so")
+LIB_PATH = os.environ.get("MOBA_LIB") or os.path.join(_HERE, "libmoba_b200.so")
 
 MOBA_OK = 0
 MOBA_ERR_SHAPE = 1

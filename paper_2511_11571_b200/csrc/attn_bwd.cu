@@ -42,7 +42,7 @@ constexpr int kDq0 = kSm0 + kSmWarps;                     // first dQ-epilogue w
 constexpr int kBwdTcThreads = 32 * (kDq0 + 4);
 
 struct BwdBars {
-    uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, s_empty, p_full, p_empty;
+    uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, p_full, p_empty;
     uint64_t dq_full, dq_empty, dkv_full, dkv_empty;
     uint32_t tmem;
 };
@@ -92,7 +92,6 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
             mbar_init(&bars->qd_empty[st], 1 + 4);   // MMA commit + dQ warps (ids read)
         }
         mbar_init(&bars->s_full, 1);
-        mbar_init(&bars->s_empty, kSmWarps);
         mbar_init(&bars->p_full, kSmWarps);
         mbar_init(&bars->p_empty, 1);
         mbar_init(&bars->dq_full, 1);
@@ -339,10 +338,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (warp == kSm0) TRACE(8);
-                if (lane == 0) {
-                    mbar_arrive(&bars->s_empty);
-                    mbar_arrive(&bars->p_full);
-                }
+                if (lane == 0) mbar_arrive(&bars->p_full);
             }
             // ---- dK, dV of this slab (zeros when no query attends); D split by half
             if (n_tiles > 0) {

@@ -6,7 +6,8 @@ import paper_2511_11571_b200 as mb
 from paper_2511_11571_b200 import _lib
 
 CFGS = {"C2": (16, 8192, 64, 128, 8, 0), "C3": (16, 32768, 64, 64, 16, 3),
-        "C4": (16, 65536, 128, 128, 8, 0), "64K": (32, 65536, 64, 128, 8, 0)}
+        "C4": (16, 65536, 128, 128, 8, 0), "64K": (32, 65536, 64, 128, 8, 0),
+        "256K": (32, 262144, 64, 128, 8, 0), "512K": (32, 524288, 64, 128, 8, 0)}
 lib = _lib.load()
 for name in (sys.argv[1:] or list(CFGS)):
     H, N, d, B, k, conv = CFGS[name]
