@@ -14,6 +14,7 @@
 //   bwd_finalize   : dQ = dQ_acc * scale -> bf16 (src/attention.py:299)
 #include "common.cuh"
 #include "sm100.cuh"
+#include <cstdio>
 #include <cstdlib>
 
 namespace moba {
@@ -204,22 +205,21 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
                 tc_fence_after();
                 fence_proxy_async_smem();
-                if (lane == 0) {
+                // warp-uniform issue (elect.sync inside the asm; a lane-0 region
+                // makes the compiler wrap every MMA in an elect/broadcast loop)
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const int sl = kk >> 2, ke = (kk & 3) * 16;
-                        umma_bf16(t_s, desc_kmajor(kb + sl * KT * 128, ke), desc_kmajor(qb + sl * MQ * 128, ke),
-                                  idesc_kq, kk > 0);
-                    }
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const int sl = kk >> 2, ke = (kk & 3) * 16;
-                        umma_bf16(t_dp, desc_kmajor(vb + sl * KT * 128, ke), desc_kmajor(db + sl * MQ * 128, ke),
-                                  idesc_kq, kk > 0);
-                    }
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const int sl = kk >> 2, ke = (kk & 3) * 16;
+                    umma_bf16_w(t_s, desc_kmajor(kb + sl * KT * 128, ke), desc_kmajor(qb + sl * MQ * 128, ke),
+                                idesc_kq, kk > 0);
                 }
-                if (lane == 0) umma_commit(&bars->s_full);
-                __syncwarp();
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const int sl = kk >> 2, ke = (kk & 3) * 16;
+                    umma_bf16_w(t_dp, desc_kmajor(vb + sl * KT * 128, ke), desc_kmajor(db + sl * MQ * 128, ke),
+                                idesc_kq, kk > 0);
+                }
+                umma_commit_w(&bars->s_full);
                 mbar_wait(&bars->p_full, g & 1);
                 TRACE(4);
                 if (!kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
@@ -227,32 +227,26 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 if (t == 0) mbar_wait(&bars->dkv_empty, (kv_use & 1) ^ 1);
                 tc_fence_after();
                 fence_proxy_async_smem();
-                if (lane == 0) {
-                    // dV += P^T dO ; dK += dS^T Q   (K = queries; P^T, dS^T bf16 in TMEM)
+                // dV += P^T dO ; dK += dS^T Q   (K = queries; P^T, dS^T bf16 in TMEM)
 #pragma unroll
-                    for (int kk = 0; kk < MQ / 16; ++kk) {
-                        const uint32_t acol = 64 * (kk >> 2) + 8 * (kk & 3);
-                        const bool acc = (t > 0) || (kk > 0);
-                        umma_bf16_ts(t_dv, t_s + acol, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, acc);
-                        umma_bf16_ts(t_dk, t_dp + acol, desc_mnmajor(qb, kk * 16, MQ * 128), idesc_kd, acc);
-                    }
-                    // dQ_tile = dS K   (M = queries from dS^T as MN-major A, K = keys)
+                for (int kk = 0; kk < MQ / 16; ++kk) {
+                    const uint32_t acol = 64 * (kk >> 2) + 8 * (kk & 3);
+                    const bool acc = (t > 0) || (kk > 0);
+                    umma_bf16_ts_w(t_dv, t_s + acol, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, acc);
+                    umma_bf16_ts_w(t_dk, t_dp + acol, desc_mnmajor(qb, kk * 16, MQ * 128), idesc_kd, acc);
+                }
+                // dQ_tile = dS K   (M = queries from dS^T as MN-major A, K = keys)
 #pragma unroll
-                    for (int kk = 0; kk < KT / 16; ++kk) {
-                        umma_bf16(t_dq, desc_mnmajor(sb, kk * 16, KT * 128), desc_mnmajor(kb, kk * 16, KT * 128),
-                                  idesc_qd, kk > 0);
-                    }
+                for (int kk = 0; kk < KT / 16; ++kk)
+                    umma_bf16_w(t_dq, desc_mnmajor(sb, kk * 16, KT * 128), desc_mnmajor(kb, kk * 16, KT * 128),
+                                idesc_qd, kk > 0);
+                umma_commit_w(&bars->dq_full);
+                umma_commit_w(&bars->p_empty);
+                umma_commit_w(&bars->qd_empty[st]);
+                if (t + 1 == n_tiles) {
+                    umma_commit_w(&bars->dkv_full);
+                    umma_commit_w(&bars->kv_empty);
                 }
-                if (lane == 0) {
-                    umma_commit(&bars->dq_full);
-                    umma_commit(&bars->p_empty);
-                    umma_commit(&bars->qd_empty[st]);
-                    if (t + 1 == n_tiles) {
-                        umma_commit(&bars->dkv_full);
-                        umma_commit(&bars->kv_empty);
-                    }
-                }
-                __syncwarp();
             }
         } else if (warp < kDq0) {
             // ------------------------------------------------ softmax-bwd (8 warps)
@@ -653,6 +647,15 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
                                                width, kv_group, counts, offsets, flat, scale, qstages, n_items, dq_acc,
                                                dq_part, part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, trp);
         st = check_launch("moba_bwd_tc_kernel");
+        if (st == 0 && tracing) {
+            static long long host[64 * 16];
+            cudaMemcpyAsync(host, tr, sizeof(host), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            if (FILE* f = std::fopen(std::getenv("MOBA_TRACE"), "wb")) {
+                std::fwrite(host, sizeof(host), 1, f);
+                std::fclose(f);
+            }
+        }
     }
     }
     if (st) return st;
