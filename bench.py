@@ -467,7 +467,7 @@ def run_ours(args, rank, world):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": float(te.item()) / args.steps,
-                "path": f"pinned host Q,K,V,dO -> moba_fwd_bwd_host (public API; {args.e2e_chunks} head chunks, "
+                "path": f"pinned host Q,K,V,dO -> moba_fwd_bwd_host (public API; {args.e2e_chunks or 'auto'} head chunks, "
                         f"H2D / one CUDA-graph replay per chunk / D2H on 3 streams) -> host O,LSE,dQ,dK,dV"},
         "gpu_launches": launches,
         "clocks": clocks,
@@ -560,7 +560,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--route-mode", choices=["fp32", "tc"], default="tc")
     ap.add_argument("--deterministic", action="store_true", help="deterministic dQ schedule")
-    ap.add_argument("--e2e-chunks", type=int, default=8, help="head chunks of the host-buffer pipeline")
+    ap.add_argument("--e2e-chunks", type=int, default=None,
+                    help="head chunks of the host-buffer pipeline (default: the API's own choice, ~32 MB of inputs each)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the sweep and the fp32-route step")
     ap.add_argument("--no-fa2", action="store_true")

@@ -196,10 +196,14 @@ def moba_fwd_bwd_host(q, k, v, do, block_size: int, top_k: int, *, n_chunks: int
     (O, LSE, dQ, dK, dV). Requires a CUDA device (no CPU fallback).
     graphs=True replays one captured CUDA graph per head chunk (captured on
     first use for each chunk shape), graphs=False launches the kernels
-    eagerly. Default 8 head chunks with graphs, 4 without (measured best for
-    16 x 8K heads on PCIe 5: graphs 2.10 / 1.99 / 2.63 ms at 4 / 8 / 16)."""
+    eagerly. Default chunking: about 32 MB of inputs per chunk, at least 4
+    chunks (measured on PCIe 5, graphs: 16 x 8K heads 1.99 / 2.05 / 2.73 ms
+    at 4 / 8 / 16 chunks; 32 x 64K heads 25.9 / 26.0 / 24.3 ms at 8 / 16 / 32
+    chunks — the last chunk's download is the exposed tail)."""
     if n_chunks is None:
-        n_chunks = 8 if graphs else 4
+        in_bytes = sum(t.numel() * t.element_size() for t in (q, k, v, do))
+        n_chunks = max(4, int(round(in_bytes / (32 << 20)))) if graphs else 4
+        n_chunks = min(n_chunks, int(q.shape[0]))
     if not torch.cuda.is_available():
         raise ConfigError("moba_fwd_bwd_host needs a CUDA device (there is no CPU fallback)")
     dev = torch.cuda.current_device()

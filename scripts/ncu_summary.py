@@ -1,6 +1,6 @@
 """Summarise ncu captures (gpurun_out/*.ncu-rep, launches.csv) into profiles/.
 
-usage: python scripts/ncu_summary.py <round-tag>
+usage: python scripts/ncu_summary.py <round-tag> [workload key, e.g. b2h16_n65536_d64]
 writes profiles/<tag>_ncu_summary.md, profiles/<tag>_launches.md and
 profiles/ncu_traffic.json (dram bytes per launch of each profiled stage,
 read by bench.py for roofline.traffic).
@@ -32,7 +32,7 @@ METRICS = [
     ("launch__shared_mem_per_block_dynamic", "dyn smem/block"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
 ]
-STAGE_OF = {"moba_bwd": "bwd", "moba_fwd": "fwd", "route_topk": "route", "combine": "combine", "bwd_preprocess": "bwd_pre", "varlen": "varlen",
+STAGE_OF = {"moba_bwd": "bwd", "moba_fwd": "fwd", "route_tc_kernel": "route", "combine": "combine", "bwd_preprocess": "bwd_pre", "varlen": "varlen",
             "centroid": "centroid"}
 
 
@@ -41,7 +41,7 @@ def to_bytes(val, unit):
     return float(val.replace(",", "")) * mul
 
 
-def main(tag):
+def main(tag, workload=None):
     os.makedirs(PROF, exist_ok=True)
     lines = [f"# ncu summary — {tag}", "",
              "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
@@ -51,6 +51,9 @@ def main(tag):
     tp = os.path.join(PROF, "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp))
+    if workload:
+        traffic = {"workload": workload,
+                   "source": f"profiles/{tag}_ncu_summary.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
     for rep in sorted(glob.glob(os.path.join(OUT, "prof_*.ncu-rep"))):
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
@@ -102,4 +105,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", sys.argv[2] if len(sys.argv) > 2 else None)
