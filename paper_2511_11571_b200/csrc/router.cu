@@ -92,9 +92,8 @@ MOBA_DEV void select_chunk32(const float (&sv)[32], int j0, int lim, float (&ts)
 }
 
 template <int D, int KMAX, typename QT>
-__global__ void __launch_bounds__(kRouteThreads)
-route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent, int64_t N,
-                       int B, int top_k, int kv_group, int32_t* __restrict__ topk) {
+MOBA_DEV void route_topk_fp32_tile(const QT* __restrict__ Q, const float* __restrict__ cent, int64_t N,
+                                   int B, int top_k, int kv_group, int32_t* __restrict__ topk, int64_t h, int tile) {
     extern __shared__ __align__(16) float route_smem[];
     float (*q_s)[kRouteQ] = reinterpret_cast<float (*)[kRouteQ]>(route_smem);
     float (*c_s)[kRouteC] = reinterpret_cast<float (*)[kRouteC]>(route_smem + D * kRouteQ);
@@ -103,11 +102,11 @@ route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent,
     int* sel_i = reinterpret_cast<int*>(sel_s + 4 * 33 * 33);
 
     const int tid = threadIdx.x;
-    const int64_t h = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * kRouteQ;
+    const int64_t r0 = (int64_t)tile * kRouteQ;
     const int n_blocks = (int)((N + B - 1) / B);
     const int width = top_k + 1;
     const QT* Qh = Q + h * N * D;
+    __syncthreads();   // a persistent CTA's previous tile is done with the shared buffers
     const float* Ch = cent + (int64_t)(h / kv_group) * n_blocks * D;   // GQA: the query head's K/V head
 
     // stage the query tile transposed (fp32, exact)
@@ -204,6 +203,25 @@ route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent,
     }
     row[nvalid] = my_own;
     for (int s = nvalid + 1; s < width; ++s) row[s] = -1;
+}
+
+
+// tiles == nullptr: one CTA per (128-query tile, head) of the grid.
+// tiles != nullptr: persistent CTAs walk the device list tiles[1 .. tiles[0]]
+// of (head * n_tiles + tile) ids — the tiles the tensor-core router could
+// not decide exactly (route_tc.cu), routed again here from scratch.
+template <int D, int KMAX, typename QT>
+__global__ void __launch_bounds__(kRouteThreads)
+route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent, int64_t N,
+                       int B, int top_k, int kv_group, int32_t* __restrict__ topk, const int* __restrict__ tiles) {
+    const int n_list = tiles != nullptr ? *tiles : 1;
+    const int n_tiles = (int)((N + kRouteQ - 1) / kRouteQ);
+    for (int li = tiles != nullptr ? (int)blockIdx.x : 0; li < n_list; li += (tiles != nullptr ? (int)gridDim.x : 1)) {
+    const int tile_id = tiles != nullptr ? tiles[1 + li] : 0;
+    route_topk_fp32_tile<D, KMAX, QT>(Q, cent, N, B, top_k, kv_group, topk,
+                                      tiles != nullptr ? tile_id / n_tiles : (int64_t)blockIdx.y,
+                                      tiles != nullptr ? tile_id % n_tiles : (int)blockIdx.x);
+    }
 }
 
 
@@ -695,6 +713,26 @@ template <int D, int KMAX>
 int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, int64_t N, int B, int top_k,
                     int32_t* topk, void* ws, cudaStream_t s);
 
+// exact fp32 re-routing of the tiles listed in `tiles` (count, then ids)
+template <int D, int KMAX>
+int launch_route_fp32_tiles(const void* q, const float* cent, int64_t bh, int kv_group, int64_t N, int B, int top_k,
+                            int32_t* topk, const int* tiles, cudaStream_t s) {
+    const size_t fsmem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
+    auto kern = route_topk_fp32_kernel<D, KMAX, __nv_bfloat16>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+    const int64_t n_tiles = bh * ceil_div(N, kRouteQ);
+    const unsigned grid = (unsigned)std::min<int64_t>(n_tiles, 2 * kNumSMs);
+    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk, tiles);
+    return check_launch("route_topk_fp32_kernel (tile list)");
+}
+#define MOBA_RF_INST(D, K)                                                                                       \
+    template int launch_route_fp32_tiles<D, K>(const void*, const float*, int64_t, int, int64_t, int, int,      \
+                                               int32_t*, const int*, cudaStream_t);
+MOBA_RF_INST(64, 1) MOBA_RF_INST(64, 2) MOBA_RF_INST(64, 4) MOBA_RF_INST(64, 8) MOBA_RF_INST(64, 16) MOBA_RF_INST(64, 32)
+MOBA_RF_INST(128, 1) MOBA_RF_INST(128, 2) MOBA_RF_INST(128, 4) MOBA_RF_INST(128, 8) MOBA_RF_INST(128, 16)
+MOBA_RF_INST(128, 32)
+#undef MOBA_RF_INST
+
 template <int D, int KMAX>
 static int launch_route(const void* q, bool q_f32, const float* cent, int64_t bh, int64_t N, int B, int top_k,
                         int mode, int kv_group, int32_t* topk, void* split_ws, cudaStream_t s) {
@@ -705,13 +743,13 @@ static int launch_route(const void* q, bool q_f32, const float* cent, int64_t bh
         if (mode != MOBA_ROUTE_FP32) return MOBA_ERR_CONFIG;
         auto kern = route_topk_fp32_kernel<D, KMAX, float>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-        kern<<<grid, kRouteThreads, fsmem, s>>>((const float*)q, cent, N, B, top_k, kv_group, topk);
+        kern<<<grid, kRouteThreads, fsmem, s>>>((const float*)q, cent, N, B, top_k, kv_group, topk, nullptr);
         return check_launch("route_topk_fp32_kernel");
     }
     if (mode == MOBA_ROUTE_TC) return launch_route_tc<D, KMAX>(q, cent, bh, kv_group, N, B, top_k, topk, split_ws, s);
     auto kern = route_topk_fp32_kernel<D, KMAX, __nv_bfloat16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk);
+    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk, nullptr);
     return check_launch("route_topk_fp32_kernel");
 }
 

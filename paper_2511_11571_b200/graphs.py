@@ -31,7 +31,11 @@ class MobaGraphedStep:
             raise ConfigError("MobaGraphedStep needs a CUDA device (there is no CPU fallback)")
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.block_size, self.top_k, self.mode, self.deterministic = block_size, top_k, mode, deterministic
-        mk = lambda: torch.zeros(tuple(shape), dtype=torch.bfloat16, device=dev)
+        # warm-up / capture inputs: seeded random values (all-zero inputs make
+        # every routing score tie, which sends every row to the exact fp32
+        # re-routing pass — correct, but a needlessly slow warm-up)
+        gen = torch.Generator(device=dev).manual_seed(0)
+        mk = lambda: torch.randn(tuple(shape), generator=gen, device=dev).to(torch.bfloat16)
         self.q, self.k, self.v, self.dout = mk().requires_grad_(True), mk().requires_grad_(True), \
             mk().requires_grad_(True), mk()
         self.conv_weight = None if conv_weight is None else conv_weight.detach().clone().requires_grad_(True)

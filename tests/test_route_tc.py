@@ -1,7 +1,7 @@
 """The tensor-core router (tcgen05 scores from a two-term bf16 split of the
 centroids, route_tc.cu) is certified against the fp32 router: its guard
 (score gap vs a per-row error bound, in-kernel exact rescoring of the k + 2
-best candidates, full fp32 reselection of queued rows) makes its plan
+best candidates, exact fp32 re-routing of undecided tiles) makes its plan
 BITWISE the fp32 router's plan — and the fp32 router is the one held to
 the reference (ties within 1e-6, tests/test_gpu_parity.py). Checked over
 shapes, GQA, key conv, exact ties (repeated key blocks) and badly scaled
@@ -67,3 +67,33 @@ def test_tc_plan_with_key_conv():
     q, kk = (torch.randn(2, 32768, 64, generator=gen, device="cuda").bfloat16() for _ in range(2))
     w = (torch.rand(3, 64, generator=gen, device="cuda") - 0.5).contiguous()
     _same(*_plans(q, kk, 64, 16, w))
+
+
+@pytest.mark.parametrize("kind", ["zeros", "constant_keys", "padded_tail"])
+def test_tc_plan_degenerate_inputs(kind):
+    """All-tie inputs (zero / constant keys, a zero-padded tail as in padded
+    training batches): every affected row is undecidable for the
+    tensor-core scores, so its tile is routed again by the exact fp32 router
+    (tile-list mode) — the plan is still bitwise the fp32 router's, and the
+    pass stays far cheaper than a per-row reselection (timed below)."""
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    H, N, d, B, k = 8, 65536, 64, 128, 8
+    q = torch.randn(H, N, d, generator=gen, device="cuda").bfloat16()
+    kk = torch.randn(H, N, d, generator=gen, device="cuda").bfloat16()
+    if kind == "zeros":
+        q.zero_()
+        kk.zero_()
+    elif kind == "constant_keys":
+        kk[:] = kk[:, :1, :]
+    else:
+        q[:, N // 2:] = 0
+        kk[:, N // 2:] = 0
+    tc, fp = _plans(q, kk, B, k)
+    _same(tc, fp)
+    cent, _ = _device.centroids(kk, B)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    _device.route(q, cent, B, k, _lib.MOBA_ROUTE_TC)
+    b.record()
+    torch.cuda.synchronize()
+    assert a.elapsed_time(b) < 50.0, f"degenerate tc routing took {a.elapsed_time(b):.1f} ms"
