@@ -17,103 +17,108 @@ constexpr int kTileM = 128;       // gathered query rows per item
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ---------------------------------------------------------------- combine
-// One warp per query: merge its vwidth = width * slabs partials
-// (lse-weighted). Virtual slot v = slot * slabs + slab lives at partial
-// position row_pos[slot] * slabs + slab; lane l owns virtual slots l, l+32,
-// l+64, l+96 (C = ceil(VW / 32) chunks). A partial row (D bf16) is read by
-// L = D/8 lanes with 16-B loads, so one warp instruction fetches 32/L
-// partial rows; all rounds are issued before any is consumed. The lane
-// groups are then reduced with shuffles and the first L lanes write the row.
-template <int D, int VW>
+// L = D/8 lanes per query (16 B of a partial row each), so a warp merges
+// 32/L queries at once (4 at d = 64, 2 at d = 128) with no cross-lane
+// reduction of the output: lane `sub` of a group owns elements
+// [8 sub, 8 sub + 8) of its query's row. Virtual slot v = slot * slabs + slab
+// lives at partial position row_pos[slot] * slabs + slab; the group's lanes
+// load the positions and LSEs of slots sub, sub + L, ... and broadcast them
+// with in-group shuffles. Every partial row of a batch of up to 16 slots is
+// requested before any is consumed. (The former one-query-per-warp layout
+// issued ~460 instructions per query and was issue bound: ncu 83% issue
+// active at N = 64K.)
+template <int D, int VW, bool kOneSlab>
 __global__ void __launch_bounds__(256)
 moba_combine_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_lse,
                     const int32_t* __restrict__ row_pos, int64_t N, int width, int slabs, int64_t total_rows,
                     __nv_bfloat16* __restrict__ O, float* __restrict__ LSE) {
-    const int vwidth = width * slabs;
-    constexpr int L = D / 8;               // lanes per partial row
-    constexpr int G = 32 / L;              // partial rows per warp instruction
-    constexpr int C = (VW + 31) / 32;      // 32-slot chunks
-    constexpr int RC = ((VW < 32 ? VW : 32) + G - 1) / G;   // load rounds per chunk
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= total_rows) return;
-    const int grp = lane / L, sub = lane % L;
-    const int64_t h = row / N;
+    constexpr int L = D / 8;                 // lanes per query
+    constexpr int QPW = 32 / L;              // queries per warp
+    constexpr int C = (VW + L - 1) / L;      // slot chunks per lane
+    constexpr int NB = VW < 16 ? VW : 16;    // partial rows in flight per lane
+    const int vwidth = kOneSlab ? width : width * slabs;
+    const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L, g0 = grp * L;
+    const int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * QPW + grp;
+    const bool ok = row < total_rows;
+    const int64_t r = ok ? row : total_rows - 1;
+    const int64_t h = total_rows < (1ll << 31) ? (int64_t)((uint32_t)r / (uint32_t)N) : r / N;
+    const float* lse_h = part_lse + h * N * vwidth;
     int32_t p[C];
     float ls[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const int v = 32 * c + lane;
-        const int32_t q = (v < vwidth) ? __ldg(row_pos + row * width + v / slabs) : -1;
-        p[c] = q >= 0 ? q * slabs + v % slabs : -1;
-        ls[c] = (p[c] >= 0) ? __ldg(part_lse + h * N * vwidth + p[c]) : -INFINITY;
+        const int v = sub + L * c;
+        const int32_t q = (v < vwidth) ? __ldg(row_pos + r * width + (kOneSlab ? v : v / slabs)) : -1;
+        p[c] = q >= 0 ? (kOneSlab ? q : q * slabs + v % slabs) : -1;
+        ls[c] = (p[c] >= 0) ? __ldg(lse_h + p[c]) : -INFINITY;
     }
-    const uint4* base = reinterpret_cast<const uint4*>(part_o + h * N * vwidth * D) + sub;
-    uint4 raw[C][RC];
-    int32_t pr[C][RC];
-    const int32_t p0 = max(__shfl_sync(0xffffffffu, p[0], 0), 0);
+    float m = ls[0];
 #pragma unroll
-    for (int c = 0; c < C; ++c)
+    for (int c = 1; c < C; ++c) m = fmaxf(m, ls[c]);
 #pragma unroll
-        for (int r = 0; r < RC; ++r) {
-            const int s = r * G + grp;                      // slot inside the chunk
-            pr[c][r] = __shfl_sync(0xffffffffu, p[c], s & 31);
-            if (s >= 32 || 32 * c + s >= vwidth) pr[c][r] = -1;
-            raw[c][r] = __ldg(base + (int64_t)(pr[c][r] >= 0 ? pr[c][r] : p0) * L);
-        }
-    float mloc = ls[0];
-#pragma unroll
-    for (int c = 1; c < C; ++c) mloc = fmaxf(mloc, ls[c]);
-    const float m = warp_max(mloc);
-    float w[C], wloc = 0.f;
+    for (int o = L / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float w[C], ws = 0.f;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         w[c] = (p[c] >= 0) ? __expf(ls[c] - m) : 0.f;
-        wloc += w[c];
+        ws += w[c];
     }
-    const float wsum = warp_sum(wloc);
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    const uint4* base = reinterpret_cast<const uint4*>(part_o + h * N * vwidth * D) + sub;
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll
-    for (int c = 0; c < C; ++c)
+    for (int v0 = 0; v0 < VW; v0 += NB) {
+        if (v0 >= vwidth) break;
+        uint4 raw[NB];
+        float wt[NB];
 #pragma unroll
-        for (int r = 0; r < RC; ++r) {
-            float wt = __shfl_sync(0xffffffffu, w[c], (r * G + grp) & 31);
-            if (pr[c][r] < 0) wt = 0.f;
-            const uint32_t u[4] = {raw[c][r].x, raw[c][r].y, raw[c][r].z, raw[c][r].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f = unpack_bf16(u[e]);
-                acc[2 * e] = fmaf(wt, f.x, acc[2 * e]);
-                acc[2 * e + 1] = fmaf(wt, f.y, acc[2 * e + 1]);
-            }
+        for (int u = 0; u < NB; ++u) {
+            const int v = v0 + u;            // compile-time: chunk v / L, held by lane g0 + v % L
+            const int32_t pv = __shfl_sync(0xffffffffu, p[v / L], g0 + v % L);
+            const float wv = __shfl_sync(0xffffffffu, w[v / L], g0 + v % L);
+            const bool live = v < vwidth && pv >= 0;
+            wt[u] = live ? wv : 0.f;
+            raw[u] = live ? __ldg(base + (int64_t)pv * L) : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
-    for (int o = L; o < 32; o <<= 1)
+        for (int u = 0; u < NB; ++u) {
+            const uint32_t uu[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-    const float inv = 1.f / wsum;
-    if (grp == 0) {
-        uint4 outv = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
-                                pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
-        *(reinterpret_cast<uint4*>(O + row * D) + sub) = outv;
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = unpack_bf16(uu[e]);
+                acc[2 * e] = fmaf(wt[u], f.x, acc[2 * e]);
+                acc[2 * e + 1] = fmaf(wt[u], f.y, acc[2 * e + 1]);
+            }
+        }
     }
-    if (lane == 0) LSE[row] = m + __logf(wsum);
+    if (!ok) return;
+    const float inv = 1.f / ws;
+    *(reinterpret_cast<uint4*>(O + row * D) + sub) =
+        make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                   pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+    if (sub == 0) LSE[row] = m + __logf(ws);
 }
 
 template <int D>
 static void launch_combine(const void* part_o, const float* part_lse, const int32_t* row_pos, int64_t N, int width,
-                           int slabs, int64_t rows, void* out, float* lse, cudaStream_t s) {
-    const unsigned grid = (unsigned)ceil_div(rows, 8);
+                           int S, int64_t rows, void* out, float* lse, cudaStream_t s) {
+    const unsigned grid = (unsigned)ceil_div(rows, 8 * (256 / D));   // 8 warps x (32 / (D / 8)) queries
     auto po = (const __nv_bfloat16*)part_o;
     auto o = (__nv_bfloat16*)out;
-    const int vw = width * slabs;
-#define MOBA_COMBINE(W) moba_combine_kernel<D, W><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, slabs, rows, o, lse)
+    const int vw = width * S;
+#define MOBA_COMBINE(W)                                                                                    \
+    (S == 1 ? moba_combine_kernel<D, W, true><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, S, rows, o, lse) \
+            : moba_combine_kernel<D, W, false><<<grid, 256, 0, s>>>(po, part_lse, row_pos, N, width, S, rows, o, lse))
+    // exact slot counts for the common widths (top-k 8 / 16 -> 9 / 17 slots)
     if (vw <= 4) MOBA_COMBINE(4);
     else if (vw <= 8) MOBA_COMBINE(8);
+    else if (vw <= 9) MOBA_COMBINE(9);
     else if (vw <= 12) MOBA_COMBINE(12);
     else if (vw <= 16) MOBA_COMBINE(16);
+    else if (vw <= 17) MOBA_COMBINE(17);
     else if (vw <= 24) MOBA_COMBINE(24);
     else if (vw <= 32) MOBA_COMBINE(32);
     else if (vw <= 64) MOBA_COMBINE(64);

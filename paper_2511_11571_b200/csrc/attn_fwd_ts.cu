@@ -92,8 +92,6 @@ MOBA_DEV void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
                  : "memory");
 }
 
-__device__ int g_fwd_trace_cta = 0;   // CTA recorded by MOBA_FWD_TRACE (MOBA_FWD_TRACE_CTA)
-
 MOBA_DEV Item load_item(const Item* p) {
     int4 v = __ldg(reinterpret_cast<const int4*>(p));
     return Item{v.x, v.y, v.z, v.w};
@@ -113,7 +111,7 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
     // debug timeline (MOBA_FWD_TRACE): CTA 0, lane 0 of the recording warp
 #define TR(li, ev)                                                                          \
     do {                                                                                    \
-        if (trace != nullptr && (int)blockIdx.x == g_fwd_trace_cta && lane == 0 && (li) < 256) trace[(li) * 16 + (ev)] = clock64(); \
+        if (trace != nullptr && blockIdx.x == 0 && lane == 0 && (li) < 256) trace[(li) * 16 + (ev)] = clock64(); \
     } while (0)
     constexpr int SL = D / 64;
     constexpr int QS = C::QS;
@@ -557,12 +555,7 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int k
     static long long* trace = nullptr;
     const char* trace_path = std::getenv("MOBA_FWD_TRACE");
     if (trace_path != nullptr && trace == nullptr) cudaMalloc(&trace, 256 * 16 * sizeof(long long));
-    if (trace_path != nullptr) {
-        cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
-        const char* tc = std::getenv("MOBA_FWD_TRACE_CTA");
-        const int cta = tc != nullptr ? std::atoi(tc) : 0;
-        cudaMemcpyToSymbolAsync(g_fwd_trace_cta, &cta, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-    }
+    if (trace_path != nullptr) cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
     {
         StageTimer tm(T_FWD, s);
         kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, kv_group, slabs, flat,
