@@ -651,6 +651,10 @@ static VarlenGeom varlen_geom(int64_t n_tokens, int block_size) {
     VarlenGeom g;
     g.n_blocks = (int)ceil_div(n_tokens, block_size);
     int64_t tq = 128;
+    // long sequences: chunks of >= n/8 queries, so the per-chunk O(n) cursor
+    // setup stays below the chunk's entries (measured: 512K 3.67 -> 3.61 ms)
+    if (g.n_blocks > 1024)
+        while (tq < g.n_blocks / 8 && tq < 4096) tq *= 2;
     while (ceil_div(n_tokens, tq) * (int64_t)g.n_blocks > (4ll << 20) && tq < (1 << 20)) tq *= 2;
     g.TQ = (int)tq;
     g.n_chunks = (int)ceil_div(n_tokens, tq);
@@ -693,7 +697,9 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     if (st) return st;
     const size_t rsmem = (size_t)g.TQ * width * sizeof(int32_t);
     const size_t ssmem4 = 4 * hsmem + rsmem;
-    if (ssmem4 <= 48 * 1024) {
+    // the 4-warp walk sets up 4 cursor rows of n blocks per chunk: worth it
+    // only while n is small (256K, n = 2048: 2.14 ms with it, 1.23 without)
+    if (ssmem4 <= 48 * 1024 && g.n_blocks <= 1024) {
         varlen_scatter4_kernel<<<dim3(g.n_chunks, (unsigned)bh), 128, ssmem4, s>>>(
             topk, N, width, g.n_blocks, g.TQ, g.n_chunks, cc, offsets, flat, row_pos);
         return check_launch("varlen_scatter4_kernel");
