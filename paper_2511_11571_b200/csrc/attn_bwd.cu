@@ -520,32 +520,57 @@ __global__ void bwd_finalize_kernel(const float* __restrict__ dq_acc, int64_t n,
 }
 
 // deterministic dQ: per query, sum its partials in (slot, slab) order.
-template <int D>
-__global__ void bwd_dq_combine_kernel(const float* __restrict__ dq_part, int64_t part_stride, int slabs,
-                                      const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t rows,
-                                      float scale, __nv_bfloat16* __restrict__ dQ) {
-    constexpr int PER = D / 32;
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const int64_t h = row / N;
-    int32_t p = (lane < width) ? row_pos[row * width + lane] : -1;
-    float acc[PER];
+// Deterministic dQ: a query's fp32 per-(query, block) partial rows summed in
+// slot order (fixed order -> bitwise reproducible). L = D/4 lanes per query
+// (16 B of the fp32 row each): 2 queries per warp at d = 64, 1 at d = 128;
+// the group's lanes load the positions of slots sub, sub + L, ... and
+// broadcast them, and every partial row of a batch of up to 16 slots is in
+// flight before any is added.
+template <int D, int W>
+__global__ void __launch_bounds__(256)
+bwd_dq_combine_kernel(const float* __restrict__ dq_part, int64_t part_stride, int slabs,
+                      const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t rows, float scale,
+                      __nv_bfloat16* __restrict__ dQ) {
+    constexpr int L = D / 4;                  // lanes per query
+    constexpr int QPW = 32 / L;
+    constexpr int C = (W + L - 1) / L;
+    constexpr int NB = W < 16 ? W : 16;
+    const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L, g0 = grp * L;
+    const int64_t row = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * QPW + grp;
+    const bool ok = row < rows;
+    const int64_t r = ok ? row : rows - 1;
+    const int64_t h = rows < (1ll << 31) ? (int64_t)((uint32_t)r / (uint32_t)N) : r / N;
+    int32_t p[C];
 #pragma unroll
-    for (int c = 0; c < PER; ++c) acc[c] = 0.f;
-    for (int s = 0; s < width; ++s) {
-        int32_t ps = __shfl_sync(0xffffffffu, p, s);
-        if (ps < 0) continue;
-        for (int sl = 0; sl < slabs; ++sl) {
-            const float* src = dq_part + sl * part_stride + (h * N * width + ps) * D + lane * PER;
+    for (int c = 0; c < C; ++c) {
+        const int sl = sub + L * c;
+        p[c] = (sl < width) ? __ldg(row_pos + r * width + sl) : -1;
+    }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int sb = 0; sb < slabs; ++sb) {
+        const float4* base = reinterpret_cast<const float4*>(dq_part + sb * part_stride + h * N * width * D) + sub;
 #pragma unroll
-            for (int c = 0; c < PER; ++c) acc[c] += src[c];
+        for (int v0 = 0; v0 < W; v0 += NB) {
+            if (v0 >= width) break;
+            float4 x[NB];
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                const int v = v0 + u;
+                const int32_t pv = __shfl_sync(0xffffffffu, p[v / L], g0 + v % L);
+                x[u] = (v < width && pv >= 0) ? __ldg(base + (int64_t)pv * (D / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                acc.x += x[u].x;
+                acc.y += x[u].y;
+                acc.z += x[u].z;
+                acc.w += x[u].w;
+            }
         }
     }
-    __nv_bfloat16* dst = dQ + row * D + lane * PER;
-#pragma unroll
-    for (int c = 0; c < PER; c += 2)
-        *reinterpret_cast<uint32_t*>(dst + c) = pack_bf16(acc[c] * scale, acc[c + 1] * scale);
+    if (!ok) return;
+    *reinterpret_cast<uint2*>(dQ + row * D + sub * 4) =
+        make_uint2(pack_bf16(acc.x * scale, acc.y * scale), pack_bf16(acc.z * scale, acc.w * scale));
 }
 
 int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* Dd,
@@ -670,8 +695,16 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         if (st) return st;
     }
     if (det) {
-        bwd_dq_combine_kernel<D><<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(dq_part, part_stride, slabs, row_pos, N,
-                                                                           width, rows, scale, (__nv_bfloat16*)dq);
+        const unsigned grid = (unsigned)ceil_div(rows, 8 * (128 / D));   // 8 warps x (32 / (D / 4)) queries
+#define MOBA_DQC(W) bwd_dq_combine_kernel<D, W><<<grid, 256, 0, s>>>(dq_part, part_stride, slabs, row_pos, N, width, \
+                                                                     rows, scale, (__nv_bfloat16*)dq)
+        if (width <= 4) MOBA_DQC(4);
+        else if (width <= 8) MOBA_DQC(8);
+        else if (width <= 9) MOBA_DQC(9);
+        else if (width <= 16) MOBA_DQC(16);
+        else if (width <= 17) MOBA_DQC(17);
+        else MOBA_DQC(32);
+#undef MOBA_DQC
         return check_launch("bwd_dq_combine_kernel");
     }
     const int64_t ne = rows * D;
