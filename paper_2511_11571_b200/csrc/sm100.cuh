@@ -77,6 +77,18 @@ MOBA_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// one try_wait with an explicit suspend-time hint (ns); true if the phase completed
+MOBA_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+        : "memory");
+    return ok != 0;
+}
 MOBA_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     if (mbar_try_wait_sleep(bar, parity)) return;
     const long long t0 = clock64();
