@@ -48,9 +48,42 @@ def _check_qkv(Q, K, V):
         raise ShapeError(f"shape mismatch: Q{tuple(Q.shape)} K{tuple(K.shape)} V{tuple(V.shape)}")
 
 
-def _prepare_plan(plan: RoutingPlan, info, cfg: MobaConfig, H: int) -> RoutingPlan:
+_PLAN_FIELDS = ("topk_indices", "counts", "offsets", "flat_queries")
+
+
+def _as_device_plan(plan, info, cfg: MobaConfig, device) -> RoutingPlan:
+    """A plan built elsewhere — e.g. the reference's own RoutingPlan dataclass
+    (src/core.py:229-251: topk_indices, counts, offsets, flat_queries as
+    numpy arrays, one head) — uploaded as this package's device plan; its
+    invariants are then checked by validate_plan like any other plan."""
+    if not all(hasattr(plan, f) for f in _PLAN_FIELDS):
+        raise PlanValidationError("plan must be a RoutingPlan (this package's, or one with the reference's "
+                                  "topk_indices / counts / offsets / flat_queries fields)")
+    try:
+        arrs = [np.asarray(getattr(plan, f)) for f in _PLAN_FIELDS]
+    except Exception as e:  # pragma: no cover - exotic array types
+        raise PlanValidationError(f"plan fields are not arrays: {e}") from None
+    topk, counts, offsets, flat = arrs
+    if topk.ndim == 2:                      # the reference's per-head plan
+        topk, counts, offsets, flat = topk[None], counts[None], offsets[None], flat[None]
+    if topk.ndim != 3 or counts.ndim != 2 or offsets.ndim != 2 or flat.ndim != 2:
+        raise PlanValidationError("plan arrays have unexpected ranks")
+    H, N, width = topk.shape
+    if N != info.n_tokens:
+        raise PlanValidationError(f"topk_indices shape {tuple(topk.shape)} does not match N={info.n_tokens}")
+    if counts.shape[0] != H or np.any(counts.astype(np.int64).sum(axis=1) != flat.shape[1]):
+        raise PlanValidationError("flat_queries length does not match sum(counts)")
+    if flat.shape[1] > N * width:
+        raise PlanValidationError("non-sentinel entry count does not match sum(counts)")
+    flat_cap = np.full((H, N * width), -1, dtype=np.int32)
+    flat_cap[:, : flat.shape[1]] = flat[:, : N * width]
+    up = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=device)
+    return RoutingPlan(up(topk), up(counts), up(offsets), up(flat_cap), None, N, cfg.block_size_B)
+
+
+def _prepare_plan(plan, info, cfg: MobaConfig, H: int, device) -> RoutingPlan:
     if not isinstance(plan, RoutingPlan):
-        raise PlanValidationError("plan must be a RoutingPlan from this package (build_plan / build_varlen)")
+        plan = _as_device_plan(plan, info, cfg, device)
     if plan.n_heads != H:
         raise PlanValidationError(f"plan has {plan.n_heads} heads, inputs have {H}")
     _device.validate(plan, info.n_tokens, cfg.block_size_B)
@@ -66,7 +99,7 @@ def moba_forward(Q, K, V, plan: RoutingPlan, cfg: MobaConfig,
     q, info = to_heads(Q, "Q")
     k, _ = to_heads(K, "K", device=q.device)
     v, _ = to_heads(V, "V", device=q.device)
-    plan = _prepare_plan(plan, info, cfg, q.shape[0])
+    plan = _prepare_plan(plan, info, cfg, q.shape[0], q.device)
     out, lse = _device.fwd(q, k, v, plan, _device.softmax_scale(info.d))
     if counters is not None:
         add_forward_counters(counters, plan, info.d, cfg, _device.visible_pairs(plan))
@@ -99,7 +132,7 @@ def moba_backward(Q, K, V, O, dO, lse, plan: RoutingPlan, cfg: MobaConfig,
     v, _ = to_heads(V, "V", device=q.device)
     o, _ = to_heads(O, "O", device=q.device)
     do, _ = to_heads(dO, "dO", device=q.device)
-    plan = _prepare_plan(plan, info, cfg, q.shape[0])
+    plan = _prepare_plan(plan, info, cfg, q.shape[0], q.device)
     dq, dk, dv = _device.bwd(q, k, v, o, do, lse_t, plan, _device.softmax_scale(info.d),
                              deterministic=(schedule == "deterministic"))
     if counters is not None:

@@ -659,3 +659,25 @@ def test_head_view_of_stale_plan_rebuilds_row_pos():
     res = mb.moba_forward(q[1:], kk[1:], v[1:], h1, cfg)
     ref = mb.moba_forward(q[1:], kk[1:], v[1:], other.head(1), cfg)
     assert torch.equal(res.output, ref.output)
+
+
+def test_moba_forward_backward_accept_reference_plan():
+    """A plan object shaped like the reference's RoutingPlan dataclass
+    (src/core.py:229-251: numpy topk_indices / counts / offsets /
+    flat_queries for one head) drives moba_forward / moba_backward exactly
+    like this package's plan; a malformed one raises PlanValidationError."""
+    from types import SimpleNamespace
+    g = load("ragged_n500_b64")
+    cfg = mb.MobaConfig(block_size_B=int(g["B"]), top_k=int(g["k"]), head_dim_d=g["Q"].shape[1])
+    ref_plan = SimpleNamespace(topk_indices=g["topk"], counts=g["counts"], offsets=g["offsets"], flat_queries=g["flat"])
+    Q, K, V = f64(g["Q"]), f64(g["K"]), f64(g["V"])
+    res = mb.moba_forward(Q, K, V, ref_plan, cfg)
+    assert_close(res.output, g["O"], "O (reference-shaped plan)")
+    assert_close(res.logsumexp, g["LSE"], "LSE (reference-shaped plan)")
+    dQ, dK, dV = mb.moba_backward(Q, K, V, res.output, f64(g["dO"]), res.logsumexp, ref_plan, cfg)
+    assert_close(dQ, g["dQ"], "dQ (reference-shaped plan)")
+    assert_close(dK, g["dK"], "dK (reference-shaped plan)")
+    assert_close(dV, g["dV"], "dV (reference-shaped plan)")
+    bad = SimpleNamespace(topk_indices=g["topk"], counts=g["counts"], offsets=g["offsets"], flat_queries=g["flat"][:-1])
+    with pytest.raises(mb.PlanValidationError):
+        mb.moba_forward(Q, K, V, bad, cfg)
