@@ -45,6 +45,7 @@
 #include "common.cuh"
 #include "sm100.cuh"
 #include <algorithm>
+#include <type_traits>
 
 namespace moba {
 namespace rtc {
@@ -54,9 +55,12 @@ constexpr int kN = 128;            // centroids per chunk (MMA N)
 constexpr int kSplits = 2;         // bf16 hi + lo terms of the fp32 centroids
 constexpr int kW = 64;             // score columns per TMEM buffer (MMA N of one sub-chunk)
 
-template <int D>
+// TT: query tiles per unit — 3 (16 warps) at d = 64, 4 (21 warps, more
+// selection warps in flight per SM) for long sequences at d = 64 (512K route
+// 24.3 -> 23.2 ms; no gain below 256K), 2 (11 warps) at d = 128
+template <int D, int TT = (D == 64) ? 3 : 2>
 struct Geo {
-    static constexpr int T = (D == 64) ? 3 : 2;          // query tiles per unit (16 / 11 warps)
+    static constexpr int T = TT;
     static constexpr int NBUF = (D == 64) ? 2 : 4;       // TMEM score buffers per tile
     static constexpr int CS = (D == 64) ? 3 : 2;         // centroid chunk smem stages
     static constexpr int kSelWarps = 4 * T;
@@ -177,14 +181,14 @@ MOBA_DEV float exact_score_g(const __nv_bfloat16* __restrict__ q, const float* _
     return acc;
 }
 
-template <int D, int KMAX>
-__global__ void __launch_bounds__(Geo<D>::kThreads, 1)
+template <int D, int KMAX, int TT>
+__global__ void __launch_bounds__(Geo<D, TT>::kThreads, 1)
 route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c,
                 const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, const float* __restrict__ cmax2,
                 int64_t N, int B, int top_k, int64_t split_rows, int kv_group, int bh, int n_tiles, int n_groups,
                 int idx_bits, int32_t* __restrict__ topk, int* __restrict__ recheck) {
     using namespace sm100;
-    using G = Geo<D>;
+    using G = Geo<D, TT>;
     constexpr int T = G::T, NBUF = G::NBUF, CS = G::CS;
     constexpr int LS = (KMAX + 4 < 32) ? KMAX + 4 : 32;
     constexpr int SL = D / 64;
@@ -597,19 +601,26 @@ int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, 
     if (!make_tmap_bf16(&tm_q, q, (uint64_t)(bh * N), D, kM) ||
         !make_tmap_bf16(&tm_c, split, (uint64_t)(2 * rows), D, kN))
         return MOBA_ERR_CUDA;
-    const int n_groups = (int)ceil_div(n_tiles, Geo<D>::T);
-    const int64_t units = bh * n_groups;
-    if (units >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
     int idx_bits = 1;
     while ((1ll << idx_bits) < n) ++idx_bits;
     if (idx_bits > 20) return MOBA_ERR_UNSUPPORTED;
-    auto kern = route_tc_kernel<D, KMAX>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<D>::kSmem);
-    const unsigned grid = (unsigned)std::min<int64_t>(units, kNumSMs);
-    kern<<<grid, Geo<D>::kThreads, Geo<D>::kSmem, s>>>(tm_q, tm_c, (const __nv_bfloat16*)q, cent, cmax2, N, B, top_k,
-                                                       rows, kv_group, (int)bh, n_tiles, n_groups, idx_bits, topk,
-                                                       recheck);
-    st = check_launch("route_tc_kernel");
+    auto go = [&](auto tt_tag) -> int {
+        constexpr int TT = decltype(tt_tag)::value;
+        using G = Geo<D, TT>;
+        const int n_groups = (int)ceil_div(n_tiles, G::T);
+        const int64_t units = bh * n_groups;
+        if (units >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
+        auto kern = route_tc_kernel<D, KMAX, TT>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
+        const unsigned grid = (unsigned)std::min<int64_t>(units, kNumSMs);
+        kern<<<grid, G::kThreads, G::kSmem, s>>>(tm_q, tm_c, (const __nv_bfloat16*)q, cent, cmax2, N, B, top_k, rows,
+                                                 kv_group, (int)bh, n_tiles, n_groups, idx_bits, topk, recheck);
+        return check_launch("route_tc_kernel");
+    };
+    if constexpr (D == 64)
+        st = (N >= (1 << 18)) ? go(std::integral_constant<int, 4>{}) : go(std::integral_constant<int, 3>{});
+    else
+        st = go(std::integral_constant<int, 2>{});
     if (st) return st;
     return launch_route_fp32_tiles<D, KMAX>(q, cent, bh, kv_group, N, B, top_k, topk, recheck, s);
 }

@@ -35,7 +35,8 @@ def _same(a, b):
 @pytest.mark.parametrize("H,N,d,B,k", [(4, 8192, 64, 128, 8), (2, 65536, 64, 128, 8), (2, 16384, 128, 128, 8),
                                        (2, 32768, 64, 64, 16), (3, 1000, 64, 32, 3), (2, 4096, 128, 256, 4),
                                        (2, 3000, 64, 16, 1), (1, 20000, 64, 32, 31), (2, 9000, 128, 64, 2),
-                                       (1, 131072, 64, 16, 8), (2, 300, 64, 128, 8), (5, 1500, 128, 32, 8)])
+                                       (1, 131072, 64, 16, 8), (2, 300, 64, 128, 8), (5, 1500, 128, 32, 8),
+                                       (1, 262144, 64, 128, 8), (1, 300000, 64, 64, 16)])
 def test_tc_plan_equals_fp32_plan(H, N, d, B, k):
     gen = torch.Generator(device="cuda").manual_seed(N + k)
     q, kk = (torch.randn(H, N, d, generator=gen, device="cuda").bfloat16() for _ in range(2))
