@@ -126,6 +126,39 @@ MOBA_DEV void key_insert2(uint32_t (&ts)[LS], uint32_t x, uint32_t y) {
     for (int u = 0; u < LS; ++u) ts[u] = nw[u];
 }
 
+// candidate (s, j) with j larger than every listed index: after every entry
+// with score >= s (ties keep the lower index first)
+template <int LS>
+MOBA_DEV void list_insert(float (&ts)[LS], int (&ti)[LS], float s, int j) {
+    bool ge[LS];
+#pragma unroll
+    for (int u = 0; u < LS; ++u) ge[u] = ts[u] >= s;
+#pragma unroll
+    for (int u = LS - 1; u >= 1; --u) {
+        const float ns = ge[u - 1] ? s : ts[u - 1];
+        const int ni = ge[u - 1] ? j : ti[u - 1];
+        ts[u] = ge[u] ? ts[u] : ns;
+        ti[u] = ge[u] ? ti[u] : ni;
+    }
+    ts[0] = ge[0] ? ts[0] : s;
+    ti[0] = ge[0] ? ti[0] : j;
+}
+
+// the same chain with q in registers
+template <int D>
+MOBA_DEV float exact_score(const float (&q)[D], const float* __restrict__ c) {
+    float acc = 0.f;
+#pragma unroll
+    for (int dd = 0; dd < D; dd += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(c + dd));
+        acc = fmaf(q[dd], v.x, acc);
+        acc = fmaf(q[dd + 1], v.y, acc);
+        acc = fmaf(q[dd + 2], v.z, acc);
+        acc = fmaf(q[dd + 3], v.w, acc);
+    }
+    return acc;
+}
+
 // (score desc, index asc)
 MOBA_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
 
@@ -524,14 +557,18 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                 }
             }
             if (status == 2) {
-                // the row's tile is routed again, whole, by the exact fp32
-                // router (route_topk_fp32_kernel in tile-list mode); the first
-                // flagging row of a tile appends it to the list
+                // queued twice: as a row (recheck[0] counts, rows after the
+                // tile flags) and, by its tile's first such row, as a tile
+                // (recheck[1] counts, ids from recheck[2]); the pass that
+                // runs picks whichever is cheaper (route_recheck_kernel /
+                // route_topk_fp32_kernel tile-list mode)
                 const int tile_id = h * n_tiles + t;
-                if (atomicExch(recheck + 1 + bh * n_tiles + tile_id, 1) == 0) {
-                    const int slot = atomicAdd(recheck, 1);
-                    recheck[1 + slot] = tile_id;
+                if (atomicExch(recheck + 2 + bh * n_tiles + tile_id, 1) == 0) {
+                    const int slot = atomicAdd(recheck + 1, 1);
+                    recheck[2 + slot] = tile_id;
                 }
+                const int rslot = atomicAdd(recheck, 1);
+                recheck[2 + 2 * bh * n_tiles + rslot] = (int)((int64_t)h * N + my_i);
             }
             if (valid) write_row<KMAX>(topk + ((int64_t)h * N + my_i) * width, res, top_k, own, width);
         }
@@ -541,6 +578,74 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
+    }
+}
+
+// Queued rows, one warp per row: every candidate j < own scored with the fp32
+// chain (lanes stride over j, so each lane sees its candidates in ascending
+// order), per-lane top-k lists, then a k-round warp merge by (score desc,
+// index asc). Bitwise the fp32 router's selection for the row.
+template <int D, int KMAX>
+__global__ void __launch_bounds__(256)
+route_recheck_kernel(const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, int64_t N, int B,
+                     int top_k, int kv_group, const int* __restrict__ recheck, int n_tiles_all,
+                     int32_t* __restrict__ topk) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    const int n_blocks = (int)((N + B - 1) / B);
+    const int width = top_k + 1;
+    // rows only while they are few per listed tile (about 16); otherwise the
+    // tile pass re-routes whole tiles
+    const int count = recheck[0] <= 16 * recheck[1] ? recheck[0] : 0;
+    const int* rows = recheck + 2 + 2 * n_tiles_all;
+    for (int r = gw; r < count; r += nw) {
+        const int64_t row = rows[r];
+        const int64_t h = row / N, i = row - h * N;
+        const int own = (int)(i / B);
+        const float* Ch = cent + (h / kv_group) * (int64_t)n_blocks * D;
+        float qv[D];
+#pragma unroll
+        for (int dd = 0; dd < D; dd += 8) {
+            float x[8];
+            ld8f(Q + row * D + dd, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) qv[dd + e] = x[e];
+        }
+        float ts[KMAX];
+        int ti[KMAX];
+#pragma unroll
+        for (int u = 0; u < KMAX; ++u) {
+            ts[u] = -INFINITY;
+            ti[u] = 0x7fffffff;
+        }
+        for (int j = lane; j < own; j += 32) list_insert<KMAX>(ts, ti, exact_score<D>(qv, Ch + (int64_t)j * D), j);
+        int res[KMAX];
+        int head = 0;
+        for (int p = 0; p < KMAX; ++p) {
+            float s = -INFINITY;
+            int ix = 0x7fffffff;
+#pragma unroll
+            for (int u = 0; u < KMAX; ++u)
+                if (u == head) {
+                    s = ts[u];
+                    ix = ti[u];
+                }
+            float bs = s;
+            int bi = ix;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (better(os, oi, bs, bi)) {
+                    bs = os;
+                    bi = oi;
+                }
+            }
+            res[p] = bi;
+            if (bi == ix && bi != 0x7fffffff) ++head;
+        }
+        if (lane == 0) write_row<KMAX>(topk + row * width, res, top_k, own, width);
     }
 }
 
@@ -569,13 +674,14 @@ __global__ void centroid_split2_kernel(const float* __restrict__ cent, int64_t r
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint32_t cols, uint32_t box_rows);
 template <int D, int KMAX>
 int launch_route_fp32_tiles(const void* q, const float* cent, int64_t bh, int kv_group, int64_t N, int B, int top_k,
-                            int32_t* topk, const int* tiles, cudaStream_t s);
+                            int32_t* topk, const int* tiles, const int* rows_count, cudaStream_t s);
 
-// workspace: [split bf16 2 x rows x D][cmax2 f32 x bh_kv][tile list: count + bh * n_tiles ids][bh * n_tiles flags]
+// workspace: [split bf16 2 x rows x D][cmax2 f32 x bh_kv]
+//            [row count, tile count, bh * n_tiles tile ids, bh * n_tiles flags, bh * N rows]
 size_t route_tc_ws_bytes(int64_t bh, int64_t N, int B) {
     const int64_t n = ceil_div(N, B);
     return align_up((size_t)2 * bh * n * 128 * 2, 256) + align_up((size_t)bh * 4, 256) +
-           align_up((size_t)(1 + 2 * bh * ceil_div(N, 128)) * 4, 256);
+           align_up((size_t)(2 + 2 * bh * ceil_div(N, 128) + bh * N) * 4, 256);
 }
 
 template <int D, int KMAX>
@@ -593,7 +699,7 @@ int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, 
     int* recheck = (int*)w;
     cudaMemsetAsync(cmax2, 0, (size_t)bh_kv * 4, s);
     const int n_tiles = (int)ceil_div(N, kM);
-    cudaMemsetAsync(recheck, 0, (size_t)(1 + 2 * bh * n_tiles) * 4, s);
+    cudaMemsetAsync(recheck, 0, (size_t)(2 + 2 * bh * n_tiles) * 4, s);
     centroid_split2_kernel<<<(unsigned)ceil_div(rows * 32, 256), 256, 0, s>>>(cent, rows, D, (int)n, split, cmax2);
     int st = check_launch("centroid_split2_kernel");
     if (st) return st;
@@ -622,7 +728,11 @@ int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, 
     else
         st = go(std::integral_constant<int, 2>{});
     if (st) return st;
-    return launch_route_fp32_tiles<D, KMAX>(q, cent, bh, kv_group, N, B, top_k, topk, recheck, s);
+    route_recheck_kernel<D, KMAX><<<kNumSMs * 2, 256, 0, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group,
+                                                              recheck, (int)(bh * n_tiles), topk);
+    st = check_launch("route_recheck_kernel");
+    if (st) return st;
+    return launch_route_fp32_tiles<D, KMAX>(q, cent, bh, kv_group, N, B, top_k, topk, recheck + 1, recheck, s);
 }
 
 #define MOBA_RTC_INST(D, K)                                                                                  \

@@ -213,8 +213,11 @@ MOBA_DEV void route_topk_fp32_tile(const QT* __restrict__ Q, const float* __rest
 template <int D, int KMAX, typename QT>
 __global__ void __launch_bounds__(kRouteThreads)
 route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent, int64_t N,
-                       int B, int top_k, int kv_group, int32_t* __restrict__ topk, const int* __restrict__ tiles) {
-    const int n_list = tiles != nullptr ? *tiles : 1;
+                       int B, int top_k, int kv_group, int32_t* __restrict__ topk, const int* __restrict__ tiles,
+                       const int* __restrict__ rows_count) {
+    // tile-list mode runs only when the undecided rows are many per listed
+    // tile (route_recheck_kernel takes them one by one otherwise)
+    const int n_list = tiles == nullptr ? 1 : (rows_count != nullptr && *rows_count <= 16 * *tiles) ? 0 : *tiles;
     const int n_tiles = (int)((N + kRouteQ - 1) / kRouteQ);
     for (int li = tiles != nullptr ? (int)blockIdx.x : 0; li < n_list; li += (tiles != nullptr ? (int)gridDim.x : 1)) {
     const int tile_id = tiles != nullptr ? tiles[1 + li] : 0;
@@ -722,18 +725,19 @@ int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, 
 // exact fp32 re-routing of the tiles listed in `tiles` (count, then ids)
 template <int D, int KMAX>
 int launch_route_fp32_tiles(const void* q, const float* cent, int64_t bh, int kv_group, int64_t N, int B, int top_k,
-                            int32_t* topk, const int* tiles, cudaStream_t s) {
+                            int32_t* topk, const int* tiles, const int* rows_count, cudaStream_t s) {
     const size_t fsmem = (size_t)(D * (kRouteQ + kRouteC) + kRouteQ * (kRouteC + 1) + 2 * 4 * 33 * 33) * sizeof(float);
     auto kern = route_topk_fp32_kernel<D, KMAX, __nv_bfloat16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     const int64_t n_tiles = bh * ceil_div(N, kRouteQ);
     const unsigned grid = (unsigned)std::min<int64_t>(n_tiles, 2 * kNumSMs);
-    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk, tiles);
+    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk, tiles,
+                                            rows_count);
     return check_launch("route_topk_fp32_kernel (tile list)");
 }
 #define MOBA_RF_INST(D, K)                                                                                       \
     template int launch_route_fp32_tiles<D, K>(const void*, const float*, int64_t, int, int64_t, int, int,      \
-                                               int32_t*, const int*, cudaStream_t);
+                                               int32_t*, const int*, const int*, cudaStream_t);
 MOBA_RF_INST(64, 1) MOBA_RF_INST(64, 2) MOBA_RF_INST(64, 4) MOBA_RF_INST(64, 8) MOBA_RF_INST(64, 16) MOBA_RF_INST(64, 32)
 MOBA_RF_INST(128, 1) MOBA_RF_INST(128, 2) MOBA_RF_INST(128, 4) MOBA_RF_INST(128, 8) MOBA_RF_INST(128, 16)
 MOBA_RF_INST(128, 32)
@@ -749,13 +753,13 @@ static int launch_route(const void* q, bool q_f32, const float* cent, int64_t bh
         if (mode != MOBA_ROUTE_FP32) return MOBA_ERR_CONFIG;
         auto kern = route_topk_fp32_kernel<D, KMAX, float>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-        kern<<<grid, kRouteThreads, fsmem, s>>>((const float*)q, cent, N, B, top_k, kv_group, topk, nullptr);
+        kern<<<grid, kRouteThreads, fsmem, s>>>((const float*)q, cent, N, B, top_k, kv_group, topk, nullptr, nullptr);
         return check_launch("route_topk_fp32_kernel");
     }
     if (mode == MOBA_ROUTE_TC) return launch_route_tc<D, KMAX>(q, cent, bh, kv_group, N, B, top_k, topk, split_ws, s);
     auto kern = route_topk_fp32_kernel<D, KMAX, __nv_bfloat16>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk, nullptr);
+    kern<<<grid, kRouteThreads, fsmem, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group, topk, nullptr, nullptr);
     return check_launch("route_topk_fp32_kernel");
 }
 
