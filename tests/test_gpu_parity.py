@@ -375,7 +375,7 @@ def test_routing_tensor_core_mode_c2_scale():
 
 
 @pytest.mark.parametrize("graphs", [False, True])
-@pytest.mark.parametrize("n_chunks", [1, 3])
+@pytest.mark.parametrize("n_chunks", [1, 3, None])
 def test_host_pipeline_matches_device_path(n_chunks, graphs):
     """moba_fwd_bwd_host (pinned host buffers, chunked over heads, copies on
     their own streams) returns bitwise the device path's results."""
