@@ -527,7 +527,7 @@ __global__ void bwd_finalize_kernel(const float* __restrict__ dq_acc, int64_t n,
 // broadcast them, and every partial row of a batch of up to 16 slots is in
 // flight before any is added.
 template <int D, int W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 bwd_dq_combine_kernel(const float* __restrict__ dq_part, int64_t part_stride, int slabs,
                       const int32_t* __restrict__ row_pos, int64_t N, int width, int64_t rows, float scale,
                       __nv_bfloat16* __restrict__ dQ) {
@@ -695,8 +695,8 @@ static int launch_bwd(const void* q, const void* k, const void* v, const void* o
         if (st) return st;
     }
     if (det) {
-        const unsigned grid = (unsigned)ceil_div(rows, 8 * (128 / D));   // 8 warps x (32 / (D / 4)) queries
-#define MOBA_DQC(W) bwd_dq_combine_kernel<D, W><<<grid, 256, 0, s>>>(dq_part, part_stride, slabs, row_pos, N, width, \
+        const unsigned grid = (unsigned)ceil_div(rows, 4 * (128 / D));   // 4 warps x (32 / (D / 4)) queries
+#define MOBA_DQC(W) bwd_dq_combine_kernel<D, W><<<grid, 128, 0, s>>>(dq_part, part_stride, slabs, row_pos, N, width, \
                                                                      rows, scale, (__nv_bfloat16*)dq)
         if (width <= 4) MOBA_DQC(4);
         else if (width <= 8) MOBA_DQC(8);
