@@ -678,7 +678,7 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     size_t hsmem = (size_t)g.n_blocks * sizeof(int);
     if (hsmem > 48 * 1024)
         cudaFuncSetAttribute(varlen_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
-    varlen_count_kernel<<<dim3(g.n_chunks, (unsigned)bh), 256, hsmem, s>>>(topk, N, width, g.n_blocks, g.TQ,
+    varlen_count_kernel<<<dim3(g.n_chunks, (unsigned)bh), 128, hsmem, s>>>(topk, N, width, g.n_blocks, g.TQ,
                                                                         g.n_chunks, cc, err);
     int st = check_launch("varlen_count_kernel");
     if (st) return st;
