@@ -1,6 +1,8 @@
-"""Forward timeline of one CTA (MOBA_FWD_TRACE with a build that honours
-MOBA_FWD_TRACE_CTA): per-item softmax intervals of the two warpgroups, how
-much of the time both run at once, and the item period."""
+"""Forward timeline of CTA 0 (MOBA_FWD_TRACE): per-item softmax intervals of
+the two warpgroups, how much of the time both run at once, and the item
+period. (A build whose TR macro selects the CTA from MOBA_FWD_TRACE_CTA and
+records slot 15 after the P-slot wait adds the softmax split; the shipped
+build records CTA 0 only — a selectable CTA cost 6% of the forward.)"""
 import os, sys, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_11571_b200 import _device
@@ -24,6 +26,7 @@ for a, b, i in zip(s_ok, p_done, rows):
 span = len(busy)
 print(f"items {len(rows)}: period {span / len(rows):.0f} clk, softmax {np.median(p_done - s_ok):.0f} clk, "
       f"both WGs busy {np.mean(busy >= 2) * 100:.1f}%, one busy {np.mean(busy == 1) * 100:.1f}%, none {np.mean(busy == 0) * 100:.1f}%")
-upto = np.median([t[i, 15] - t[i, 8] for i in rows if t[i, 15]])
-post = np.median([t[i, 9] - t[i, 15] for i in rows if t[i, 15]])
-print(f"softmax split: load + max + p_free wait {upto:.0f}, exp + sums + P store {post:.0f} clk")
+if any(t[i, 15] for i in rows):
+    upto = np.median([t[i, 15] - t[i, 8] for i in rows if t[i, 15]])
+    post = np.median([t[i, 9] - t[i, 15] for i in rows if t[i, 15]])
+    print(f"softmax split: load + max + p_free wait {upto:.0f}, exp + sums + P store {post:.0f} clk")
