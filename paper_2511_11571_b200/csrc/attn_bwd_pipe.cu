@@ -123,13 +123,24 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                      int B, int width, const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
                      const int32_t* __restrict__ flat, float scale, int n_items, int* __restrict__ sched,
                      float* __restrict__ dq_acc, float* __restrict__ dq_part, int64_t part_stride,
-                     __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, long long* __restrict__ trace) {
+                     __nv_bfloat16* __restrict__ dK, __nv_bfloat16* __restrict__ dV, long long* __restrict__ trace,
+                     int trace_g0) {
     using namespace sm100;
-    // debug timeline (MOBA_BWD_TRACE): CTA 0, lane 0 of the recording warp, per tile g
+    // debug timeline (MOBA_BWD_TRACE): CTA 0, lane 0 of the recording warp,
+    // tiles [trace_g0, trace_g0 + 256) of the CTA (MOBA_BWD_TRACE_G0)
+#ifdef MOBA_TIMELINE
 #define TRB(g, ev)                                                                          \
     do {                                                                                    \
-        if (trace != nullptr && blockIdx.x == 0 && lane == 0 && (g) < 256) trace[(g) * 16 + (ev)] = clock64(); \
+        if (trace != nullptr && blockIdx.x == 0 && lane == 0 && (unsigned)((g) - trace_g0) < 256u) \
+            trace[((g) - trace_g0) * 16 + (ev)] = clock64();                                \
     } while (0)
+#else
+    // compiled out of the product build (the recording branches cost 2-4%;
+    // make EXTRA=-DMOBA_TIMELINE for timelines)
+    (void)trace;
+    (void)trace_g0;
+#define TRB(g, ev) do { } while (0)
+#endif
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -485,6 +496,38 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 mbar_wait(&bars->dq_full[g & 1], (g >> 1) & 1);
                 if (warp == kEp0) TRB(g, 11);
                 tc_fence_after();
+                if (t + 1 == x.n_tiles) {
+                    mbar_wait(&bars->dkv_full, kv_use & 1);
+                    tc_fence_after();
+                    const bool live = row < x.klen;
+                    __nv_bfloat16* dk_row = dK + (x.h * N + x.kb0 + row) * D;
+                    __nv_bfloat16* dv_row = dV + (x.h * N + x.kb0 + row) * D;
+#pragma unroll
+                    for (int which = 0; which < 2; ++which) {
+                        float a[64];
+                        const uint32_t col = which ? cDK : cDV;
+                        tmem_ld32(tmem + col + lane_off, *reinterpret_cast<float(*)[32]>(&a[0]));
+                        tmem_ld32(tmem + col + 32 + lane_off, *reinterpret_cast<float(*)[32]>(&a[32]));
+                        tmem_ld_wait();
+                        if (which == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&bars->dkv_empty);
+                        }
+                        const float mul = which ? scale : 1.f;
+                        __nv_bfloat16* dst = which ? dk_row : dv_row;
+                        if (live) {
+#pragma unroll
+                            for (int c = 0; c < 8; ++c)
+                                *reinterpret_cast<uint4*>(dst + 8 * c) =
+                                    make_uint4(pack_bf16(a[8 * c] * mul, a[8 * c + 1] * mul),
+                                               pack_bf16(a[8 * c + 2] * mul, a[8 * c + 3] * mul),
+                                               pack_bf16(a[8 * c + 4] * mul, a[8 * c + 5] * mul),
+                                               pack_bf16(a[8 * c + 6] * mul, a[8 * c + 7] * mul));
+                        }
+                    }
+                    ++kv_use;
+                }
                 const int qi = lds32i(ldi_addr(st) + 1024 + row * 4);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->qd_empty[st]);
@@ -523,37 +566,10 @@ moba_bwd_pipe_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* _
                 }
                 if (warp == kEp0) TRB(g, 12);
             }
-            // dK (scaled), dV of the slab; zeros when no query attends the block
-            const bool live = row < x.klen;
-            __nv_bfloat16* dk_row = dK + (x.h * N + x.kb0 + row) * D;
-            __nv_bfloat16* dv_row = dV + (x.h * N + x.kb0 + row) * D;
-            if (x.n_tiles > 0) {
-                mbar_wait(&bars->dkv_full, kv_use & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int which = 0; which < 2; ++which) {
-                    float a[64];
-                    const uint32_t col = which ? cDK : cDV;
-                    tmem_ld32(tmem + col + lane_off, *reinterpret_cast<float(*)[32]>(&a[0]));
-                    tmem_ld32(tmem + col + 32 + lane_off, *reinterpret_cast<float(*)[32]>(&a[32]));
-                    tmem_ld_wait();
-                    const float mul = which ? scale : 1.f;
-                    __nv_bfloat16* dst = which ? dk_row : dv_row;
-                    if (live) {
-#pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            *reinterpret_cast<uint4*>(dst + 8 * c) =
-                                make_uint4(pack_bf16(a[8 * c] * mul, a[8 * c + 1] * mul),
-                                           pack_bf16(a[8 * c + 2] * mul, a[8 * c + 3] * mul),
-                                           pack_bf16(a[8 * c + 4] * mul, a[8 * c + 5] * mul),
-                                           pack_bf16(a[8 * c + 6] * mul, a[8 * c + 7] * mul));
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->dkv_empty);
-                ++kv_use;
-            } else if (live) {
+            // dK (scaled) and dV are zero when no query attends the block
+            if (x.n_tiles == 0 && row < x.klen) {
+                __nv_bfloat16* dk_row = dK + (x.h * N + x.kb0 + row) * D;
+                __nv_bfloat16* dv_row = dV + (x.h * N + x.kb0 + row) * D;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     *reinterpret_cast<uint4*>(dk_row + 8 * c) = make_uint4(0, 0, 0, 0);
@@ -599,7 +615,8 @@ int launch_bwd_pipe(const void* q, const void* k, const void* v, const void* dou
     kern<<<grid, kThreads, kSmem, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, tm_k, tm_v, lse, Dd, bh, hg,
                                        kv_group, N, B, width, counts, offsets, flat, scale, (int)n_items, sched, dq_acc, dq_part,
                                        part_stride, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv,
-                                       trace_path != nullptr ? trace : nullptr);
+                                       trace_path != nullptr ? trace : nullptr,
+                                       std::getenv("MOBA_BWD_TRACE_G0") ? std::atoi(std::getenv("MOBA_BWD_TRACE_G0")) : 0);
     int st = check_launch("moba_bwd_pipe_kernel");
     if (st == 0 && trace_path != nullptr) {
         static long long host[256 * 16];

@@ -105,14 +105,23 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                    const int32_t* __restrict__ flat, const Item* __restrict__ items,
                    const int32_t* __restrict__ item_lo, const int32_t* __restrict__ item_hi, float scale_log2,
                    __nv_bfloat16* __restrict__ part_o, float* __restrict__ part_lse,
-                   const __grid_constant__ CUtensorMap tm_po, long long* __restrict__ trace) {
+                   const __grid_constant__ CUtensorMap tm_po, long long* __restrict__ trace, int trace_cta) {
     using namespace sm100;
     using C = Cfg<D>;
-    // debug timeline (MOBA_FWD_TRACE): CTA 0, lane 0 of the recording warp
+    // debug timeline (MOBA_FWD_TRACE): CTA trace_cta (MOBA_FWD_TRACE_CTA,
+    // default 0), lane 0 of the recording warp, its first 256 items
+#ifdef MOBA_TIMELINE
 #define TR(li, ev)                                                                          \
     do {                                                                                    \
-        if (trace != nullptr && blockIdx.x == 0 && lane == 0 && (li) < 256) trace[(li) * 16 + (ev)] = clock64(); \
+        if (trace != nullptr && blockIdx.x == trace_cta && lane == 0 && (li) < 256)         \
+            trace[(li) * 16 + (ev)] = clock64();                                            \
     } while (0)
+#else
+    // compiled out of the product build (make EXTRA=-DMOBA_TIMELINE for timelines)
+    (void)trace;
+    (void)trace_cta;
+#define TR(li, ev) do { } while (0)
+#endif
     constexpr int SL = D / 64;
     constexpr int QS = C::QS;
     constexpr int NC = NCH * 32;
@@ -607,7 +616,8 @@ int launch_fwd_ts(const void* q, const void* k, const void* v, int64_t bh, int k
         StageTimer tm(T_FWD, s);
         kern<<<grid, kThreads, smem, s>>>((const __nv_bfloat16*)q, tm_k, tm_v, N, B, BP, width, kv_group, slabs, flat,
                                           (const Item*)items, item_lo, item_hi, scale_log2, (__nv_bfloat16*)part_o,
-                                          part_lse, tm_po, trace_path != nullptr ? trace : nullptr);
+                                          part_lse, tm_po, trace_path != nullptr ? trace : nullptr,
+                                          std::getenv("MOBA_FWD_TRACE_CTA") ? std::atoi(std::getenv("MOBA_FWD_TRACE_CTA")) : 0);
     }
     int st = check_launch("moba_fwd_ts_kernel");
     if (st == 0 && trace_path != nullptr) {

@@ -14,6 +14,9 @@ os.environ["MOBA_FWD_TRACE"] = path
 _device.fwd(q, kk, v, plan, d ** -0.5)
 torch.cuda.synchronize()
 t = np.fromfile(path, dtype=np.int64).reshape(256, 16)
+if not t.any():
+    sys.exit("empty timeline: the product build compiles the recording out; build a timeline "
+             "library (scripts/README.md: make -C var/tl/csrc EXTRA=-DMOBA_TIMELINE) and point MOBA_LIB at it")
 t0 = t[t > 0].min()
 names = ["mma:q_wait0", "mma:q_ok", "mma:p_wait0", "mma:p_ok", "pr:qe_wait0", "pr:qe_ok", "pr:issued",
          "sm:s_wait0", "sm:s_ok", "sm:p_done", "sm:o_ok", "sm:epi_done", "mma:pv_iss", "mma:s_iss", "sm:o_ld", "sm:s_free"]
