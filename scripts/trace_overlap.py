@@ -1,8 +1,8 @@
 """Forward timeline of CTA 0 (MOBA_FWD_TRACE): per-item softmax intervals of
 the two warpgroups, how much of the time both run at once, and the item
-period. (A build whose TR macro selects the CTA from MOBA_FWD_TRACE_CTA and
-records slot 15 after the P-slot wait adds the softmax split; the shipped
-build records CTA 0 only — a selectable CTA cost 6% of the forward.)"""
+period. Needs a timeline build (scripts/README.md, -DMOBA_TIMELINE; the
+recording is compiled out of the product library); MOBA_FWD_TRACE_CTA picks
+the CTA."""
 import os, sys, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_11571_b200 import _device
@@ -17,6 +17,8 @@ os.environ["MOBA_FWD_TRACE"] = "/tmp/fwd_ov.bin"
 _device.fwd(q, kk, v, plan, d ** -0.5)
 torch.cuda.synchronize()
 t = np.fromfile("/tmp/fwd_ov.bin", dtype=np.int64).reshape(256, 16)
+if not t.any():
+    sys.exit("empty timeline: build the library with -DMOBA_TIMELINE (scripts/README.md)")
 rows = [i for i in range(40, 200) if t[i, 8] and t[i, 9]]
 s_ok, p_done = t[rows, 8], t[rows, 9]
 busy = np.zeros(int(p_done.max() - s_ok.min()) + 1, dtype=np.int8)
