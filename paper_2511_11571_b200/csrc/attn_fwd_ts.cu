@@ -238,6 +238,7 @@ moba_fwd_ts_kernel(const __nv_bfloat16* __restrict__ Q, const __grid_constant__ 
                 mbar_arrive(&bars->q_full[qs]);
                 if (pw == 0) TR(li, 6);
                 if (li + 1 < n_local) load_ids(nxt, qrow);
+                if (pw == 0) TR(li, 15);
                 cur = nxt;
             }
     };

@@ -17,7 +17,7 @@ torch.cuda.synchronize()
 t = np.fromfile(path, dtype=np.int64).reshape(256, 16)
 if not t.any():
     sys.exit("empty timeline: the product build compiles the recording out; build a timeline "
-             "library (scripts/README.md: make -C var/tl/csrc EXTRA=-DMOBA_TIMELINE) and point MOBA_LIB at it")
+             "library (scripts/README.md: make -C var_tl/csrc EXTRA=-DMOBA_TIMELINE) and point MOBA_LIB at it")
 t0 = t[t > 0].min()
 names = ["P:qe_wait0", "P:qe_ok", "P:issued", "M:s_issue", "M:p_ok", "M:mma_done", "S:s_wait0", "S:s_ok",
          "S:A_done", "S:dp_ok", "S:B_done", "E:dq_ok", "E:done", "M:dvdk", "M:dq"]
