@@ -494,7 +494,20 @@ varlen_scatter4_kernel(const int32_t* __restrict__ topk, int64_t N, int width, i
     const int64_t i0 = (int64_t)chunk * TQ;
     const int nq = (int)(min64(i0 + TQ, N) - i0);
     const int32_t* tk = topk + (h * N + i0) * width;
-    for (int e = tid; e < nq * width; e += blockDim.x) rows_s[e] = __ldg(tk + e);
+    // the chunk's rows, 4 loads in flight per thread (one dependent load per
+    // iteration left the CTA waiting on ~9 serial global round trips)
+    {
+        const int ne = nq * width;
+        int e = tid;
+        for (; e + 3 * 128 < ne; e += 4 * 128) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(tk + e + u * 128);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rows_s[e + u * 128] = v[u];
+        }
+        for (; e < ne; e += 128) rows_s[e] = __ldg(tk + e);
+    }
     for (int b = tid; b < 4 * n_blocks; b += blockDim.x) cursor[b] = 0;
     __syncthreads();
     const int q4 = (nq + 3) / 4;
@@ -506,14 +519,25 @@ varlen_scatter4_kernel(const int32_t* __restrict__ topk, int64_t N, int width, i
     }
     __syncthreads();
     const int32_t* ccc = cc + (h * n_chunks + chunk) * (int64_t)n_blocks;
-    for (int b = tid; b < n_blocks; b += blockDim.x) {
-        int32_t run = offsets[h * n_blocks + b] + ccc[b];
+    const int32_t* offh = offsets + h * n_blocks;
+    auto place = [&](int b, int32_t run) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const int32_t c = cursor[w * n_blocks + b];
             cursor[w * n_blocks + b] = run;
             run += c;
         }
+    };
+    {
+        int b = tid;
+        for (; b + 3 * 128 < n_blocks; b += 4 * 128) {
+            int32_t r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) r[u] = __ldg(offh + b + u * 128) + __ldg(ccc + b + u * 128);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) place(b + u * 128, r[u]);
+        }
+        for (; b < n_blocks; b += 128) place(b, __ldg(offh + b) + __ldg(ccc + b));
     }
     __syncthreads();
     int32_t* fl = flat + h * N * width;
