@@ -36,14 +36,14 @@ constexpr float kLog2eB = 1.4426950408889634f;
 #define TRACE(slot) do { if (trace && blockIdx.x == 0 && lane == 0 && g < 64) trace[(g) * 16 + (slot)] = clock64(); } while (0)
 
 constexpr int kSmWarps = 8;                               // softmax-bwd warps
-constexpr int kPrWarps = 4;                               // producer (gather) warps
+constexpr int kPrWarps = 3;                               // producer (gather) warps (16 warps: 128 registers)
 constexpr int kMmaWarp = kPrWarps;                        // MMA issuer warp index
 constexpr int kSm0 = kPrWarps + 1;                        // first softmax warp
 constexpr int kDq0 = kSm0 + kSmWarps;                     // first dQ-epilogue warp
 constexpr int kBwdTcThreads = 32 * (kDq0 + 4);
 
 struct BwdBars {
-    uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, p_full, p_empty;
+    uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, p_full, p_empty, pa_full, dp_full;
     uint64_t dq_full, dq_empty, dkv_full, dkv_empty;
     uint32_t tmem;
 };
@@ -94,6 +94,8 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
         }
         mbar_init(&bars->s_full, 1);
         mbar_init(&bars->p_full, kSmWarps);
+        mbar_init(&bars->pa_full, kSmWarps);
+        mbar_init(&bars->dp_full, 1);
         mbar_init(&bars->p_empty, 1);
         mbar_init(&bars->dq_full, 1);
         mbar_init(&bars->dq_empty, 4);
@@ -105,8 +107,14 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars->tmem;
-    const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
-    const uint32_t t_dq = kDqAlias ? tmem : tmem + 256 + 2 * D;
+    // S^T and dP^T swap their 128-column regions every tile: S^T(g+1) goes
+    // where dP^T / dS^T(g) were (free once dK(g) has issued), so it no longer
+    // waits for the epilogue to drain dQ(g), which aliases S^T(g)'s region;
+    // only dP^T(g+1) does
+    auto t_s_of = [&](int gg) { return tmem + (uint32_t)(gg & 1) * 128; };
+    auto t_dp_of = [&](int gg) { return tmem + (uint32_t)((gg & 1) ^ 1) * 128; };
+    const uint32_t t_dv = tmem + 256, t_dk = tmem + 256 + D;
+    auto t_dq_of = [&](int gg) { return kDqAlias ? t_s_of(gg) : tmem + 256 + 2 * D; };
 
     auto stage_ptr = [&](int st) { return stage0 + st * stage_bytes; };
 
@@ -151,12 +159,28 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 constexpr int CPR = D / 8;                       // 16-B chunks per row
                 const int sub = lane % 8, rsub = lane / 8;
                 // warp p gathers rows 4*(p + kPrWarps*i) + rsub
-                constexpr int NI = MQ / 4 / kPrWarps;
+                constexpr int NI = (MQ / 4 + kPrWarps - 1) / kPrWarps;
                 int qrow[NI];
 #pragma unroll
                 for (int i = 0; i < NI; ++i) {
                     const int r = 4 * (warp + kPrWarps * i) + rsub;
-                    qrow[i] = (r < rows) ? fl[t * MQ + r] : -1;
+                    qrow[i] = (r < rows && r < MQ) ? fl[t * MQ + r] : -1;
+                }
+                // per-row vectors (query id, L, D) of rows 32 (p + kPrWarps i) + l,
+                // loaded before the stage wait: their dependent loads (id ->
+                // L, D) stay off the gather's critical path
+                constexpr int NV = (MQ + 32 * kPrWarps - 1) / (32 * kPrWarps);
+                int qv[NV];
+                float lv[NV], dv[NV];
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const int r = 32 * (warp + kPrWarps * i) + lane;
+                    qv[i] = (r < rows && r < MQ) ? fl[t * MQ + r] : -1;
+                }
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    lv[i] = (qv[i] >= 0) ? lse[h * N + qv[i]] * kLog2eB : 0.f;
+                    dv[i] = (qv[i] >= 0) ? Dd[h * N + qv[i]] : 0.f;
                 }
                 mbar_wait(&bars->qd_empty[st], ((g / qstages) & 1) ^ 1);
                 if (warp == 0) TRACE(0);
@@ -165,6 +189,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 #pragma unroll
                 for (int i = 0; i < NI; ++i) {
                     const int r = 4 * (warp + kPrWarps * i) + rsub, qi = qrow[i];
+                    if (r >= MQ) continue;
                     const int64_t src = (h * N + max(qi, 0)) * D;
 #pragma unroll
                     for (int c = sub; c < CPR; c += 8) {
@@ -174,13 +199,14 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                     }
                 }
                 cpasync_arrive_noinc(&bars->qd_full[st]);
-                // per-row vectors: warps 0..3, lane l write row 32 p + l
-                if (warp < MQ / 32) {
-                    const int r = 32 * warp + lane;
-                    const int qi = (r < rows) ? fl[t * MQ + r] : -1;
-                    sts32(id_a + r * 4, (uint32_t)qi);
-                    sts32(l_a + r * 4, __float_as_uint((qi >= 0) ? lse[h * N + qi] * kLog2eB : 0.f));
-                    sts32(d_a + r * 4, __float_as_uint((qi >= 0) ? Dd[h * N + qi] : 0.f));
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const int r = 32 * (warp + kPrWarps * i) + lane;
+                    if (r < MQ) {
+                        sts32(id_a + r * 4, (uint32_t)qv[i]);
+                        sts32(l_a + r * 4, __float_as_uint(lv[i]));
+                        sts32(d_a + r * 4, __float_as_uint(dv[i]));
+                    }
                 }
                 mbar_arrive(&bars->qd_full[st]);
                 if (warp == 0) TRACE(1);
@@ -196,49 +222,59 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
             for (int t = 0; t < n_tiles; ++t, ++g) {
                 const int st = g % qstages;
                 const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
+                const uint32_t t_s = t_s_of(g), t_dp = t_dp_of(g);
                 mbar_wait(&bars->qd_full[st], (g / qstages) & 1);
                 TRACE(2);
-                // P^T / dS^T of the previous tile live in the S^T / dP^T columns
-                // until its dV / dK / dQ MMAs complete (committed to dq_full)
-                if (g > 0) mbar_wait(&bars->dq_full, (g - 1) & 1);
-                TRACE(3);
-                if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
                 tc_fence_after();
                 fence_proxy_async_smem();
                 // warp-uniform issue (elect.sync inside the asm; a lane-0 region
-                // makes the compiler wrap every MMA in an elect/broadcast loop)
+                // makes the compiler wrap every MMA in an elect/broadcast loop).
+                // S^T(g) lands where dS^T(g-1) was: tcgen05.mma runs in issue
+                // order, so dK(g-1) has read it by then
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const int sl = kk >> 2, ke = (kk & 3) * 16;
                     umma_bf16_w(t_s, desc_kmajor(kb + sl * KT * 128, ke), desc_kmajor(qb + sl * MQ * 128, ke),
                                 idesc_kq, kk > 0);
                 }
+                umma_commit_w(&bars->s_full);
+                TRACE(3);
+                // dP^T(g) lands where dQ(g-1) was: wait for its drain
+                if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
+                tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const int sl = kk >> 2, ke = (kk & 3) * 16;
                     umma_bf16_w(t_dp, desc_kmajor(vb + sl * KT * 128, ke), desc_kmajor(db + sl * MQ * 128, ke),
                                 idesc_kq, kk > 0);
                 }
-                umma_commit_w(&bars->s_full);
-                mbar_wait(&bars->p_full, g & 1);
-                TRACE(4);
-                if (!kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
-                TRACE(5);
+                umma_commit_w(&bars->dp_full);
                 if (t == 0) mbar_wait(&bars->dkv_empty, (kv_use & 1) ^ 1);
+                // dV += P^T dO as soon as phase A has stored P^T (runs under phase B)
+                mbar_wait(&bars->pa_full, g & 1);
+                TRACE(4);
                 tc_fence_after();
-                fence_proxy_async_smem();
-                // dV += P^T dO ; dK += dS^T Q   (K = queries; P^T, dS^T bf16 in TMEM)
 #pragma unroll
                 for (int kk = 0; kk < MQ / 16; ++kk) {
                     const uint32_t acol = 64 * (kk >> 2) + 8 * (kk & 3);
-                    const bool acc = (t > 0) || (kk > 0);
-                    umma_bf16_ts_w(t_dv, t_s + acol, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, acc);
-                    umma_bf16_ts_w(t_dk, t_dp + acol, desc_mnmajor(qb, kk * 16, MQ * 128), idesc_kd, acc);
+                    umma_bf16_ts_w(t_dv, t_s + acol, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, (t > 0) || (kk > 0));
                 }
-                // dQ_tile = dS K   (M = queries from dS^T as MN-major A, K = keys)
+                mbar_wait(&bars->p_full, g & 1);
+                if (!kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
+                TRACE(5);
+                tc_fence_after();
+                fence_proxy_async_smem();
+                // dK += dS^T Q   (K = queries; dS^T bf16 in TMEM)
+#pragma unroll
+                for (int kk = 0; kk < MQ / 16; ++kk) {
+                    const uint32_t acol = 64 * (kk >> 2) + 8 * (kk & 3);
+                    umma_bf16_ts_w(t_dk, t_dp + acol, desc_mnmajor(qb, kk * 16, MQ * 128), idesc_kd, (t > 0) || (kk > 0));
+                }
+                // dQ_tile = dS K   (M = queries from dS^T as MN-major A, K = keys),
+                // over S^T(g) / P^T(g) (read by phase A and the dV MMAs above)
 #pragma unroll
                 for (int kk = 0; kk < KT / 16; ++kk)
-                    umma_bf16_w(t_dq, desc_mnmajor(sb, kk * 16, KT * 128), desc_mnmajor(kb, kk * 16, KT * 128),
+                    umma_bf16_w(t_dq_of(g), desc_mnmajor(sb, kk * 16, KT * 128), desc_mnmajor(kb, kk * 16, KT * 128),
                                 idesc_qd, kk > 0);
                 umma_commit_w(&bars->dq_full);
                 umma_commit_w(&bars->p_empty);
@@ -263,6 +299,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
             for (int t = 0; t < n_tiles; ++t, ++g) {
                 const int st = g % qstages;
                 const uint32_t l_a = smem_u32(stage_ptr(st)) + 2 * qt_bytes, d_a = l_a + MQ * 4, id_a = d_a + MQ * 4;
+                const uint32_t t_s = t_s_of(g), t_dp = t_dp_of(g);
                 mbar_wait(&bars->s_full, g & 1);
                 if (warp == kSm0) TRACE(6);
                 tc_fence_after();
@@ -270,63 +307,83 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 // tile-uniform: slices are ascending, so if the first query is
                 // at or past the slab's last key no element of the tile is masked
                 const bool need_mask = rows_t < MQ || klen < KT || (int64_t)lds32i(id_a) < kb0 + KT - 1;
-                mbar_wait(&bars->p_empty, (g & 1) ^ 1);
-                if (warp == kSm0) TRACE(7);
-                // the mask test is a template argument, not a branch inside the
-                // unrolled loop (per-group branches serialise the loads and
-                // exponentials); padded rows carry id -1, dead key rows never pass
+                // padded rows carry id -1, dead key rows never pass
                 const int kmask = krow_ok ? (int)key : 0x7fffffff;
-                auto run_chunks = [&](auto mask_tag) {
+                // phase A: P = exp2(S^T scale log2e - L) kept in fp32 for phase
+                // B; bf16 pairs over the S^T columns just read (A of dV).
+                // The mask test is a template argument, not a branch inside
+                // the unrolled loop (per-group branches serialise the loads
+                // and exponentials)
+                float pv[64];
+                auto phase_a = [&](auto mask_tag) {
                     constexpr bool kMask = decltype(mask_tag)::value;
-#pragma unroll 1
+#pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         const int c0 = half * 64 + c * 16;
-                        float sv[16], dpv[16];
+                        float sv[16];
                         tmem_ld16(t_s + lane_off + c0, sv);
-                        tmem_ld16(t_dp + lane_off + c0, dpv);
                         tmem_ld_wait();
-                        uint32_t pk[8], dk[8];
+                        uint32_t pk[8];
 #pragma unroll
                         for (int i = 0; i < 16; i += 4) {
                             const float4 lv = lds128f(l_a + (c0 + i) * 4);
-                            const float4 dv = lds128f(d_a + (c0 + i) * 4);
                             const float la[4] = {lv.x, lv.y, lv.z, lv.w};
-                            const float da[4] = {dv.x, dv.y, dv.z, dv.w};
-                            float pv[4], dsv[4];
+                            float* p4 = &pv[c * 16 + i];
                             if constexpr (kMask) {
                                 const int4 iv = lds128i(id_a + (c0 + i) * 4);
                                 const int ia[4] = {iv.x, iv.y, iv.z, iv.w};
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
                                     const float e = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
-                                    pv[u] = kmask <= ia[u] ? e : 0.f;
+                                    p4[u] = kmask <= ia[u] ? e : 0.f;
                                 }
                             } else {
 #pragma unroll
-                                for (int u = 0; u < 4; ++u) pv[u] = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
+                                for (int u = 0; u < 4; ++u) p4[u] = fast_exp2(fmaf(sv[i + u], sl2, -la[u]));
                             }
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) dsv[u] = pv[u] * (dpv[i + u] - da[u]);
-                            pk[i >> 1] = pack_bf16(pv[0], pv[1]);
-                            pk[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
-                            dk[i >> 1] = pack_bf16(dsv[0], dsv[1]);
-                            dk[(i >> 1) + 1] = pack_bf16(dsv[2], dsv[3]);
+                            pk[i >> 1] = pack_bf16(p4[0], p4[1]);
+                            pk[(i >> 1) + 1] = pack_bf16(p4[2], p4[3]);
                         }
-                        // P^T, dS^T (bf16 pairs) back into the S^T / dP^T columns just read
-                        // (A operands of the dV / dK MMAs); dS^T also to smem for dQ
                         tmem_st8(t_s + lane_off + half * 64 + c * 8, pk);
-                        tmem_st8(t_dp + lane_off + half * 64 + c * 8, dk);
-#pragma unroll
-                        for (int gq = 0; gq < 2; ++gq) {
-                            const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
-                            sts128(ds_a + off, make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]));
-                        }
                     }
                 };
                 if (need_mask)
-                    run_chunks(std::true_type{});
+                    phase_a(std::true_type{});
                 else
-                    run_chunks(std::false_type{});
+                    phase_a(std::false_type{});
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->pa_full);
+                // phase B: dS^T = P (dP^T - D) -> bf16 pairs over the dP^T
+                // columns (A of dK) and the SW128 smem tile (A of dQ), which
+                // the dQ MMA of the previous tile has finished reading (p_empty)
+                mbar_wait(&bars->p_empty, (g & 1) ^ 1);
+                mbar_wait(&bars->dp_full, g & 1);
+                if (warp == kSm0) TRACE(7);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int c0 = half * 64 + c * 16;
+                    float dpv[16];
+                    tmem_ld16(t_dp + lane_off + c0, dpv);
+                    tmem_ld_wait();
+                    uint32_t dk[8];
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        const float4 dv = lds128f(d_a + (c0 + i) * 4);
+                        const float da[4] = {dv.x, dv.y, dv.z, dv.w};
+                        const float* p4 = &pv[c * 16 + i];
+                        dk[i >> 1] = pack_bf16(p4[0] * (dpv[i] - da[0]), p4[1] * (dpv[i + 1] - da[1]));
+                        dk[(i >> 1) + 1] = pack_bf16(p4[2] * (dpv[i + 2] - da[2]), p4[3] * (dpv[i + 3] - da[3]));
+                    }
+                    tmem_st8(t_dp + lane_off + half * 64 + c * 8, dk);
+#pragma unroll
+                    for (int gq = 0; gq < 2; ++gq) {
+                        const uint32_t off = sw128_off(row, c0 + gq * 8, KT);
+                        sts128(ds_a + off, make_uint4(dk[4 * gq], dk[4 * gq + 1], dk[4 * gq + 2], dk[4 * gq + 3]));
+                    }
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 fence_proxy_async_smem();
@@ -391,7 +448,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 #pragma unroll
                     for (int c0 = 0; c0 < D; c0 += 32) {
                         float v[32];
-                        tmem_ld32(t_dq + lane_off + c0, v);
+                        tmem_ld32(t_dq_of(g) + lane_off + c0, v);
                         tmem_ld_wait();
                         if (qi >= 0) {
                             if (dq_part != nullptr) {
@@ -418,7 +475,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 #pragma unroll
                         for (int c0 = 0; c0 < D; c0 += 32) {
                             float v[32];
-                            tmem_ld32(t_dq + lane_off + c0, v);
+                            tmem_ld32(t_dq_of(g) + lane_off + c0, v);
                             tmem_ld_wait();
                             if (mine) {
 #pragma unroll
@@ -446,7 +503,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
 #pragma unroll
                 for (int c0 = 0; c0 < D; c0 += 32) {
                     float v[32];
-                    tmem_ld32(t_dq + lane_off + c0, v);
+                    tmem_ld32(t_dq_of(g) + lane_off + c0, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int i = 0; i < 32; i += 4)

@@ -16,7 +16,7 @@ _device.bwd(q, kk, v, o, do, lse, plan, d ** -0.5, deterministic=False)
 torch.cuda.synchronize()
 t = np.fromfile(path, dtype=np.int64).reshape(64, 16)
 t0 = t[t > 0].min()
-names = ["P:qe_ok", "P:issued", "M:qd_ok", "M:dq_prev", "M:p_ok", "M:dqe_ok", "S:s_ok", "S:pe_ok", "S:done",
+names = ["P:qe_ok", "P:issued", "M:qd_ok", "M:s_iss", "M:pa_ok", "M:p_ok", "S:s_ok", "S:dp_ok", "S:done",
          "E:dq_ok", "E:done"]
 print("g   " + " ".join(f"{n:>10s}" for n in names))
 rows = [i for i in range(64) if t[i].any()]
