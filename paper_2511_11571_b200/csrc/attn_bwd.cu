@@ -43,7 +43,10 @@ constexpr int kDq0 = kSm0 + kSmWarps;                     // first dQ-epilogue w
 constexpr int kBwdTcThreads = 32 * (kDq0 + 4);
 
 struct BwdBars {
-    uint64_t kv_full, kv_empty, qd_full[2], qd_empty[2], s_full, p_full, p_empty, pa_full, dp_full;
+    // a stage's dO half is released after dV (do_empty), its Q half (with the
+    // per-row id / L / D vectors) after dK / dQ and the epilogue's id reads
+    uint64_t kv_full, kv_empty, q_full[2], q_empty[2], do_full[2], do_empty[2], s_full, p_full, p_empty, pa_full,
+        dp_full;
     uint64_t dq_full, dq_empty, dkv_full, dkv_empty;
     uint32_t tmem;
 };
@@ -89,8 +92,10 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
         mbar_init(&bars->kv_full, 1);
         mbar_init(&bars->kv_empty, 1);
         for (int st = 0; st < 2; ++st) {
-            mbar_init(&bars->qd_full[st], 2 * 32 * kPrWarps);   // cp.async (noinc) + plain arrivals per producer lane
-            mbar_init(&bars->qd_empty[st], 1 + 4);   // MMA commit + dQ warps (ids read)
+            mbar_init(&bars->q_full[st], 2 * 32 * kPrWarps);    // cp.async (noinc) + plain arrivals per producer lane
+            mbar_init(&bars->do_full[st], 2 * 32 * kPrWarps);
+            mbar_init(&bars->q_empty[st], 1 + 4);    // MMA commit + dQ warps (ids read)
+            mbar_init(&bars->do_empty[st], 1);       // MMA commit after dV
         }
         mbar_init(&bars->s_full, 1);
         mbar_init(&bars->p_full, kSmWarps);
@@ -182,23 +187,29 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                     lv[i] = (qv[i] >= 0) ? lse[h * N + qv[i]] * kLog2eB : 0.f;
                     dv[i] = (qv[i] >= 0) ? Dd[h * N + qv[i]] : 0.f;
                 }
-                mbar_wait(&bars->qd_empty[st], ((g / qstages) & 1) ^ 1);
-                if (warp == 0) TRACE(0);
                 const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
                 const uint32_t l_a = qb + 2 * qt_bytes, d_a = l_a + MQ * 4, id_a = d_a + MQ * 4;
+                // dO rows first: their half of the stage frees once dV of the
+                // previous tile has run, while phase B and dK / dQ still read Q
+                auto gather = [&](uint32_t base, const __nv_bfloat16* src_t) {
 #pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    const int r = 4 * (warp + kPrWarps * i) + rsub, qi = qrow[i];
-                    if (r >= MQ) continue;
-                    const int64_t src = (h * N + max(qi, 0)) * D;
+                    for (int i = 0; i < NI; ++i) {
+                        const int r = 4 * (warp + kPrWarps * i) + rsub, qi = qrow[i];
+                        if (r >= MQ) continue;
+                        const int64_t src = (h * N + max(qi, 0)) * D;
 #pragma unroll
-                    for (int c = sub; c < CPR; c += 8) {
-                        const uint32_t off = sw128_off(r, c * 8, MQ);
-                        cp_async16(qb + off, Q + src + c * 8, qi >= 0);
-                        cp_async16(db + off, dO + src + c * 8, qi >= 0);
+                        for (int c = sub; c < CPR; c += 8)
+                            cp_async16(base + sw128_off(r, c * 8, MQ), src_t + src + c * 8, qi >= 0);
                     }
-                }
-                cpasync_arrive_noinc(&bars->qd_full[st]);
+                };
+                mbar_wait(&bars->do_empty[st], ((g / qstages) & 1) ^ 1);
+                gather(db, dO);
+                cpasync_arrive_noinc(&bars->do_full[st]);
+                mbar_arrive(&bars->do_full[st]);
+                mbar_wait(&bars->q_empty[st], ((g / qstages) & 1) ^ 1);
+                if (warp == 0) TRACE(0);
+                gather(qb, Q);
+                cpasync_arrive_noinc(&bars->q_full[st]);
 #pragma unroll
                 for (int i = 0; i < NV; ++i) {
                     const int r = 32 * (warp + kPrWarps * i) + lane;
@@ -208,7 +219,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                         sts32(d_a + r * 4, __float_as_uint(dv[i]));
                     }
                 }
-                mbar_arrive(&bars->qd_full[st]);
+                mbar_arrive(&bars->q_full[st]);
                 if (warp == 0) TRACE(1);
             }
         } else if (warp == kMmaWarp) {
@@ -223,7 +234,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 const int st = g % qstages;
                 const uint32_t qb = smem_u32(stage_ptr(st)), db = qb + qt_bytes;
                 const uint32_t t_s = t_s_of(g), t_dp = t_dp_of(g);
-                mbar_wait(&bars->qd_full[st], (g / qstages) & 1);
+                mbar_wait(&bars->q_full[st], (g / qstages) & 1);
                 TRACE(2);
                 tc_fence_after();
                 fence_proxy_async_smem();
@@ -241,7 +252,9 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 TRACE(3);
                 // dP^T(g) lands where dQ(g-1) was: wait for its drain
                 if (kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
+                mbar_wait(&bars->do_full[st], (g / qstages) & 1);
                 tc_fence_after();
+                fence_proxy_async_smem();
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const int sl = kk >> 2, ke = (kk & 3) * 16;
@@ -259,6 +272,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                     const uint32_t acol = 64 * (kk >> 2) + 8 * (kk & 3);
                     umma_bf16_ts_w(t_dv, t_s + acol, desc_mnmajor(db, kk * 16, MQ * 128), idesc_kd, (t > 0) || (kk > 0));
                 }
+                umma_commit_w(&bars->do_empty[st]);      // dP^T and dV have read dO
                 mbar_wait(&bars->p_full, g & 1);
                 if (!kDqAlias) mbar_wait(&bars->dq_empty, (g & 1) ^ 1);
                 TRACE(5);
@@ -278,7 +292,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                                 idesc_qd, kk > 0);
                 umma_commit_w(&bars->dq_full);
                 umma_commit_w(&bars->p_empty);
-                umma_commit_w(&bars->qd_empty[st]);
+                umma_commit_w(&bars->q_empty[st]);
                 if (t + 1 == n_tiles) {
                     umma_commit_w(&bars->dkv_full);
                     umma_commit_w(&bars->kv_empty);
@@ -441,7 +455,7 @@ moba_bwd_tc_kernel(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __r
                 tc_fence_after();
                 const int qi = lds32i(id_a + row * 4);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->qd_empty[st]);   // ids read: stage may be refilled
+                if (lane == 0) mbar_arrive(&bars->q_empty[st]);    // ids read: the Q half may be refilled
                 const int r_in = t * MQ + row;
                 if constexpr (!kStage) {
                     // no room for a staging buffer: vector reductions straight from registers
