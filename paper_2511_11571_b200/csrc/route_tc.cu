@@ -186,6 +186,15 @@ MOBA_DEV void write_row(int32_t* out, int (&res)[KMAX], int top_k, int own, int 
 
 
 
+// m += bit when s >= thr: FSETP + a predicated IMAD (one * bit + m, `one` a
+// register ptxas cannot prove to be 1, so the add stays an IMAD on the FMA
+// pipe instead of an IADD3 / SEL on the ALU)
+MOBA_DEV void filter_add(uint32_t& m, float s, float thr, uint32_t one, uint32_t bit) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\t@p mad.lo.u32 %0, %3, %4, %0;\n\t}\n"
+        : "+r"(m)
+        : "f"(s), "f"(thr), "r"(one), "r"(bit));
+}
+
 // the lane's next pending hit of the group: its staged score (lane-private
 // row at stg, 16-B chunks XOR-swizzled by sx4) and its key-index field; the
 // no-op key source (score unused, idx 0 with key 0) when none is left
@@ -367,6 +376,7 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const uint32_t sxor = (uint32_t)(lane & 7), sx4 = sxor << 4;
         const uint32_t imask = (1u << idx_bits) - 1u;
         const float gstep = ldexpf(1.f, idx_bits - 22);   // key grid step / 2^exponent (x2 margin)
+        const uint32_t one = (uint32_t)min(n_tiles, 1);      // 1 (n_tiles >= 1), opaque to ptxas
         int qcnt = 0, scnt[NBUF];
 #pragma unroll
         for (int b = 0; b < NBUF; ++b) scnt[b] = 0;
@@ -453,8 +463,17 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                                     key_insert2<LS>(ts, max(k0, k1), min(k0, k1));
                                 }
                             } else {
+                                // hit bit e: one FSETP (ALU) and a predicated
+                                // add of the bit (IMAD.IADD, FMA pipe) — the
+                                // selection is ALU bound, and SEL + IADD3
+                                // would put both halves on the ALU
+                                uint32_t m0 = 0u, m1 = 0u;
 #pragma unroll
-                                for (int e = 0; e < 16; ++e) m |= (sv[e] >= thr) ? (1u << (16 * hh + e)) : 0u;
+                                for (int e = 0; e < 16; e += 2) {
+                                    filter_add(m0, sv[e], thr, one, 1u << (16 * hh + e));
+                                    filter_add(m1, sv[e + 1], thr, one, 1u << (16 * hh + e + 1));
+                                }
+                                m |= m0 + m1;
 #pragma unroll
                                 for (int e = 0; e < 16; e += 4)
                                     sts128(stg + ((((uint32_t)(16 * hh + e) >> 2) ^ sxor) << 4),
