@@ -236,8 +236,8 @@ route_topk_fp32_kernel(const QT* __restrict__ Q, const float* __restrict__ cent,
 //            blocks -> cc[h][chunk][b]
 //  scan    : per (head, block) exclusive scan over chunks (in place) and
 //            counts[b]; then offsets = exclusive scan over blocks
-//  scatter : per (head, chunk) one warp walks its queries in ascending
-//            order, lanes = row slots; a row never repeats a block, so the
+//  scatter : per (head, chunk) warps walk their runs of the chunk's
+//            queries in ascending order, lanes = row slots; a row never repeats a block, so the
 //            per-block cursors in shared memory are conflict free and each
 //            block's slice comes out strictly ascending (src/router.py:145-148).
 
@@ -476,89 +476,113 @@ varlen_scatter_kernel(const int32_t* __restrict__ topk, int64_t N, int width, in
     for (int e = tid; e < nq * width; e += blockDim.x) rp[e] = rows_s[e];
 }
 
-// Same output as varlen_scatter_kernel with the chunk's queries split over
-// the CTA's 4 warps: each warp histograms its quarter of the rows, the
-// per-block cursors of warp w start after warps < w, and the 4 warps walk
-// their quarters concurrently (the single walking warp was the critical
-// path: 36 dependent steps per 128-query chunk).
-__global__ void __launch_bounds__(128)
-varlen_scatter4_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int n_blocks, int TQ,
-                       int n_chunks, const int32_t* __restrict__ cc, const int32_t* __restrict__ offsets,
-                       int32_t* __restrict__ flat, int32_t* __restrict__ row_pos) {
+// Wide-chunk scatter: chunks of up to 2048 queries walked by W warps at once
+// (a warp per contiguous run of the chunk's rows). The per-warp cursors are
+// 16-bit offsets relative to the chunk's 32-bit base per block, two warps
+// per shared word (warp 2i in the low half, 2i+1 in the high half; a chunk
+// holds <= 16384 queries, so no half carries into the other), so the
+// chunk setup is (1 + W/2) words per block instead of W, amortised over
+// 4-16x more entries than a 128-query chunk; each warp then walks its rows
+// in ascending order (src/router.py:143-148).
+template <int W>
+__global__ void __launch_bounds__(32 * W)
+varlen_scatter_w_kernel(const int32_t* __restrict__ topk, int64_t N, int width, int n_blocks, int TQ,
+                        int n_chunks, const int32_t* __restrict__ cc, const int32_t* __restrict__ offsets,
+                        int32_t* __restrict__ flat, int32_t* __restrict__ row_pos) {
+    constexpr int NT = 32 * W, P = W / 2;
     extern __shared__ int32_t vsm[];
-    int32_t* cursor = vsm;                   // [4][n_blocks]
-    int32_t* rows_s = vsm + 4 * n_blocks;    // [TQ * width]
+    __shared__ int n_hi_s;                                            // 1 + the chunk's largest block
+    const int n4 = (n_blocks + 3) & ~3;
+    uint32_t* rel = reinterpret_cast<uint32_t*>(vsm);                 // [P][n4]
+    int32_t* base = vsm + P * n4;                                     // [n_blocks]
+    int32_t* rows_s = base + n4;                                      // [TQ * width]
     const int64_t h = blockIdx.y;
     const int chunk = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t i0 = (int64_t)chunk * TQ;
     const int nq = (int)(min64(i0 + TQ, N) - i0);
+    const int ne = nq * width;
     const int32_t* tk = topk + (h * N + i0) * width;
-    // the chunk's rows, 4 loads in flight per thread (one dependent load per
-    // iteration left the CTA waiting on ~9 serial global round trips)
     {
-        const int ne = nq * width;
         int e = tid;
-        for (; e + 3 * 128 < ne; e += 4 * 128) {
-            int v[4];
+        for (; e + 7 * NT < ne; e += 8 * NT) {
+            int v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldg(tk + e + u * 128);
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(tk + e + u * NT);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) rows_s[e + u * 128] = v[u];
+            for (int u = 0; u < 8; ++u) rows_s[e + u * NT] = v[u];
         }
-        for (; e < ne; e += 128) rows_s[e] = __ldg(tk + e);
+        for (; e < ne; e += NT) rows_s[e] = __ldg(tk + e);
     }
-    for (int b = tid; b < 4 * n_blocks; b += blockDim.x) cursor[b] = 0;
+    for (int b = tid; b < P * n4 / 4; b += NT) reinterpret_cast<uint4*>(rel)[b] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) n_hi_s = 0;
     __syncthreads();
-    const int q4 = (nq + 3) / 4;
-    const int e_lo = min(nq, warp * q4) * width, e_hi = min(nq, (warp + 1) * q4) * width;
-    int32_t* cur = cursor + warp * n_blocks;
+    const int qw = (nq + W - 1) / W;
+    const int e_lo = min(nq, warp * qw) * width, e_hi = min(nq, (warp + 1) * qw) * width;
+    uint32_t* my = rel + (warp >> 1) * n4;
+    const int sh = (warp & 1) * 16;
+    int bmax = -1;
     for (int e = e_lo + lane; e < e_hi; e += 32) {
         const int32_t b = rows_s[e];
-        if (b >= 0) atomicAdd(&cur[b], 1);
+        if (b >= 0) atomicAdd(&my[b], 1u << sh);
+        bmax = max(bmax, b);
     }
+    bmax = __reduce_max_sync(0xffffffffu, bmax);
+    if (lane == 0) atomicMax(&n_hi_s, bmax + 1);
     __syncthreads();
+    // per block the chunk touches (causal plans: blocks <= the chunk's last
+    // query block): the chunk's base, then each warp's exclusive offset
+    const int n_hi = n_hi_s;
     const int32_t* ccc = cc + (h * n_chunks + chunk) * (int64_t)n_blocks;
     const int32_t* offh = offsets + h * n_blocks;
-    auto place = [&](int b, int32_t run) {
+    for (int b0 = tid; b0 < n_hi; b0 += 4 * NT) {
+        int32_t r[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int32_t c = cursor[w * n_blocks + b];
-            cursor[w * n_blocks + b] = run;
-            run += c;
+        for (int u = 0; u < 4; ++u) {
+            const int b = b0 + u * NT;
+            r[u] = b < n_hi ? __ldg(offh + b) + __ldg(ccc + b) : 0;
         }
-    };
-    {
-        int b = tid;
-        for (; b + 3 * 128 < n_blocks; b += 4 * 128) {
-            int32_t r[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) r[u] = __ldg(offh + b + u * 128) + __ldg(ccc + b + u * 128);
+        for (int u = 0; u < 4; ++u) {
+            const int b = b0 + u * NT;
+            if (b < n_hi) {
+                base[b] = r[u];
+                uint32_t w[P];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) place(b + u * 128, r[u]);
+                for (int p = 0; p < P; ++p) w[p] = rel[p * n4 + b];
+                uint32_t run = 0;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const uint32_t lo = w[p] & 0xffffu;
+                    rel[p * n4 + b] = run | ((run + lo) << 16);
+                    run += lo + (w[p] >> 16);
+                }
+            }
         }
-        for (; b < n_blocks; b += 128) place(b, __ldg(offh + b) + __ldg(ccc + b));
     }
     __syncthreads();
+    // the walk: one row per step, lane = slot. A row never repeats a block,
+    // so the lanes of a step hit distinct cursors (no match / rank step);
+    // consecutive steps are ordered by the warp's in-order shared atomics
     int32_t* fl = flat + h * N * width;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
-        const int e = e0 + lane;
-        const int32_t b = (e < e_hi) ? rows_s[e] : -1;
-        const unsigned grp = __match_any_sync(0xffffffffu, b);
-        int32_t p = -1;
-        if (b >= 0) {
-            p = cur[b] + __popc(grp & lt);
-            fl[p] = (int32_t)(i0 + e / width);
+    const int r_lo = e_lo / width, r_hi = e_hi / width;
+#pragma unroll 4
+    for (int r = r_lo; r < r_hi; ++r) {
+        if (lane < width) {
+            const int e = r * width + lane;
+            const int32_t b = rows_s[e];
+            int32_t p = -1;
+            if (b >= 0) {
+                const uint32_t old = atomicAdd(&my[b], 1u << sh);
+                p = base[b] + (int32_t)((old >> sh) & 0xffffu);
+                fl[p] = (int32_t)(i0 + r);
+            }
+            rows_s[e] = p;
         }
-        __syncwarp();
-        if (b >= 0 && (grp & lt) == 0) cur[b] += __popc(grp);   // group leader advances the cursor
-        if (e < e_hi) rows_s[e] = p;
-        __syncwarp();
     }
     __syncthreads();
     int32_t* rp = row_pos + (h * N + i0) * width;
-    for (int e = tid; e < nq * width; e += blockDim.x) rp[e] = rows_s[e];
+    for (int e = tid; e < ne; e += NT) rp[e] = rows_s[e];
 }
 
 // row_pos from an arbitrary (validated) plan: binary search of query i in
@@ -674,14 +698,22 @@ struct VarlenGeom {
     int n_blocks;
 };
 
+constexpr size_t kVarlenSmem = 227 * 1024 - 64;   // + the kernel's static word
+
+// chunk size the wide scatter grows towards: n/2 queries, clamped to
+// [512, 2048] (measured, b2 x h16 d64 B128 k8: 64K 512 -> 0.174 ms, 256K
+// 1024 -> 0.65 ms, 512K 2048 -> 1.58 ms; smaller chunks repeat the O(n)
+// cursor setup more often, larger ones leave too few CTAs per SM)
+static int64_t varlen_tq_target(int n_blocks) {
+    return std::min<int64_t>(2048, std::max<int64_t>(512, n_blocks / 2));
+}
+
+// workspace geometry (an upper bound on the chunk count: run_varlen may only
+// grow the chunks)
 static VarlenGeom varlen_geom(int64_t n_tokens, int block_size) {
     VarlenGeom g;
     g.n_blocks = (int)ceil_div(n_tokens, block_size);
     int64_t tq = 128;
-    // long sequences: chunks of >= n/8 queries, so the per-chunk O(n) cursor
-    // setup stays below the chunk's entries (measured: 512K 3.67 -> 3.61 ms)
-    if (g.n_blocks > 1024)
-        while (tq < g.n_blocks / 8 && tq < 4096) tq *= 2;
     while (ceil_div(n_tokens, tq) * (int64_t)g.n_blocks > (4ll << 20) && tq < (1 << 20)) tq *= 2;
     g.TQ = (int)tq;
     g.n_chunks = (int)ceil_div(n_tokens, tq);
@@ -697,6 +729,23 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     if (ws_bytes < need) return MOBA_ERR_WORKSPACE;
     int* err = (int*)ws;
     int32_t* cc = (int32_t*)((char*)ws + 256);
+    // wide-chunk scatter: the most walking warps whose cursor words fit,
+    // then chunks grown from the workspace geometry (fewer chunks only shrink
+    // cc) towards varlen_tq_target while the grid keeps >= 2 CTAs per SM
+    auto wide_smem = [&](int64_t tq, int w) {
+        return ((size_t)(1 + w / 2) * ((g.n_blocks + 3) & ~3) + (size_t)tq * width) * sizeof(int32_t);
+    };
+    int W = 16;
+    while (W > 2 && wide_smem(g.TQ, W) > kVarlenSmem) W /= 2;
+    if (g.TQ > 16384 || wide_smem(g.TQ, W) > kVarlenSmem) W = 0;
+    if (W > 0) {
+        const int64_t target = varlen_tq_target(g.n_blocks);
+        int64_t tq = g.TQ;
+        while (tq < target && bh * ceil_div(N, 2 * tq) >= 2 * kNumSMs && wide_smem(2 * tq, W) <= kVarlenSmem)
+            tq *= 2;
+        g.TQ = (int)tq;
+        g.n_chunks = (int)ceil_div(N, tq);
+    }
     StageTimer tm(T_VARLEN, s);
     cudaMemsetAsync(err, 0, sizeof(int), s);
     size_t hsmem = (size_t)g.n_blocks * sizeof(int);
@@ -722,16 +771,25 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
         st = check_launch("varlen_scan_kernel");
     }
     if (st) return st;
-    const size_t rsmem = (size_t)g.TQ * width * sizeof(int32_t);
-    const size_t ssmem4 = 4 * hsmem + rsmem;
-    // the 4-warp walk sets up 4 cursor rows of n blocks per chunk: worth it
-    // only while n is small (256K, n = 2048: 2.14 ms with it, 1.23 without)
-    if (ssmem4 <= 48 * 1024 && g.n_blocks <= 1024) {
-        varlen_scatter4_kernel<<<dim3(g.n_chunks, (unsigned)bh), 128, ssmem4, s>>>(
-            topk, N, width, g.n_blocks, g.TQ, g.n_chunks, cc, offsets, flat, row_pos);
-        return check_launch("varlen_scatter4_kernel");
+    if (W > 0) {
+        const size_t wsmem = wide_smem(g.TQ, W);
+        switch (W) {
+#define MOBA_SCATTER_W(w)                                                                                       \
+    case w:                                                                                                     \
+        cudaFuncSetAttribute(varlen_scatter_w_kernel<w>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem); \
+        varlen_scatter_w_kernel<w><<<dim3(g.n_chunks, (unsigned)bh), 32 * w, wsmem, s>>>(                      \
+            topk, N, width, g.n_blocks, g.TQ, g.n_chunks, cc, offsets, flat, row_pos);                          \
+        break;
+            MOBA_SCATTER_W(16)
+            MOBA_SCATTER_W(8)
+            MOBA_SCATTER_W(4)
+            MOBA_SCATTER_W(2)
+#undef MOBA_SCATTER_W
+        }
+        return check_launch("varlen_scatter_w_kernel");
     }
-    const size_t ssmem = hsmem + rsmem;
+    // capacity fallback (the per-warp cursor words do not fit): one walking warp
+    const size_t ssmem = hsmem + (size_t)g.TQ * width * sizeof(int32_t);
     if (ssmem > 48 * 1024) {
         if (ssmem > 227 * 1024) return MOBA_ERR_UNSUPPORTED;
         cudaFuncSetAttribute(varlen_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
