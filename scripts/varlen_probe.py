@@ -3,7 +3,7 @@
 usage: python scripts/varlen_probe.py [N ...]   (32 heads, d=64, B=128, top-k 8)
 Times moba_varlen alone (CUDA events, 20 launches) for each N and checks
 flat / row_pos / counts / offsets against a torch.sort of the (block, query)
-pairs. MOBA_VARLEN_TQ (comma list) sweeps the chunk target.
+pairs.
 """
 import ctypes
 import os
@@ -35,7 +35,6 @@ def reference_plan(topk, n):
 
 def main():
     Ns = [int(x) for x in sys.argv[1:]] or [8192, 65536, 262144, 524288]
-    tqs = os.environ.get("MOBA_VARLEN_TQ", "2048").split(",")
     lib = _lib.load()
     H, D, B, K = 32, 64, 128, 8
     torch.manual_seed(0)
@@ -60,8 +59,7 @@ def main():
                                  flat.data_ptr(), row_pos.data_ptr(), ws.data_ptr(), ws.numel(), s)
             _lib.check(st, "moba_varlen")
 
-        for tq in tqs:
-            os.environ["MOBA_VARLEN_TQ"] = tq
+        for _rep in range(1):
             for _ in range(3):
                 run()
             torch.cuda.synchronize()
@@ -85,7 +83,7 @@ def main():
                     if not torch.equal(offsets[h], torch.cumsum(rc, 0).int() - rc):
                         ok = f"MISMATCH offsets head {h}"
                         break
-            print(f"N={N} tq_target={tq} varlen {ms:.4f} ms  {ok}", flush=True)
+            print(f"N={N} varlen {ms:.4f} ms  {ok}", flush=True)
 
 
 if __name__ == "__main__":
