@@ -696,6 +696,7 @@ struct VarlenGeom {
     int TQ;
     int n_chunks;
     int n_blocks;
+    int W;   // walking warps of the wide-chunk scatter (0: the one-warp capacity fallback)
 };
 
 constexpr size_t kVarlenSmem = 227 * 1024 - 64;   // + the kernel's static word
@@ -708,13 +709,31 @@ static int64_t varlen_tq_target(int n_blocks) {
     return std::min<int64_t>(2048, std::max<int64_t>(512, n_blocks / 2));
 }
 
-// workspace geometry (an upper bound on the chunk count: run_varlen may only
-// grow the chunks)
-static VarlenGeom varlen_geom(int64_t n_tokens, int block_size) {
+static size_t varlen_wide_smem(int64_t tq, int w, int n_blocks, int width) {
+    return ((size_t)(1 + w / 2) * ((n_blocks + 3) & ~3) + (size_t)tq * width) * sizeof(int32_t);
+}
+
+// The chunk geometry of one varlen call (the workspace query uses the same
+// function, so the chunk-count matrix it sizes is exact): chunks of >= 128
+// queries with at most 4M chunk-count entries per head; then, for the wide
+// scatter, the most walking warps whose cursor words fit in shared memory
+// and chunks grown towards varlen_tq_target while the grid keeps >= 2 CTAs
+// per SM.
+static VarlenGeom varlen_geom(int64_t bh, int64_t n_tokens, int block_size, int width) {
     VarlenGeom g;
     g.n_blocks = (int)ceil_div(n_tokens, block_size);
     int64_t tq = 128;
     while (ceil_div(n_tokens, tq) * (int64_t)g.n_blocks > (4ll << 20) && tq < (1 << 20)) tq *= 2;
+    int W = 16;
+    while (W > 2 && varlen_wide_smem(tq, W, g.n_blocks, width) > kVarlenSmem) W /= 2;
+    if (tq > 16384 || varlen_wide_smem(tq, W, g.n_blocks, width) > kVarlenSmem) W = 0;
+    if (W > 0) {
+        const int64_t target = varlen_tq_target(g.n_blocks);
+        while (tq < target && bh * ceil_div(n_tokens, 2 * tq) >= 2 * kNumSMs &&
+               varlen_wide_smem(2 * tq, W, g.n_blocks, width) <= kVarlenSmem)
+            tq *= 2;
+    }
+    g.W = W;
     g.TQ = (int)tq;
     g.n_chunks = (int)ceil_div(n_tokens, tq);
     return g;
@@ -723,29 +742,13 @@ static VarlenGeom varlen_geom(int64_t n_tokens, int block_size) {
 static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int B, int32_t* counts,
                       int32_t* offsets, int32_t* flat, int32_t* row_pos, void* ws, size_t ws_bytes,
                       cudaStream_t s, bool sync_range_check) {
-    VarlenGeom g = varlen_geom(N, B);
+    const VarlenGeom g = varlen_geom(bh, N, B, width);
     if (g.n_blocks > 16384) return MOBA_ERR_UNSUPPORTED;
     size_t need = 256 + (size_t)bh * g.n_chunks * g.n_blocks * sizeof(int32_t);
     if (ws_bytes < need) return MOBA_ERR_WORKSPACE;
     int* err = (int*)ws;
     int32_t* cc = (int32_t*)((char*)ws + 256);
-    // wide-chunk scatter: the most walking warps whose cursor words fit,
-    // then chunks grown from the workspace geometry (fewer chunks only shrink
-    // cc) towards varlen_tq_target while the grid keeps >= 2 CTAs per SM
-    auto wide_smem = [&](int64_t tq, int w) {
-        return ((size_t)(1 + w / 2) * ((g.n_blocks + 3) & ~3) + (size_t)tq * width) * sizeof(int32_t);
-    };
-    int W = 16;
-    while (W > 2 && wide_smem(g.TQ, W) > kVarlenSmem) W /= 2;
-    if (g.TQ > 16384 || wide_smem(g.TQ, W) > kVarlenSmem) W = 0;
-    if (W > 0) {
-        const int64_t target = varlen_tq_target(g.n_blocks);
-        int64_t tq = g.TQ;
-        while (tq < target && bh * ceil_div(N, 2 * tq) >= 2 * kNumSMs && wide_smem(2 * tq, W) <= kVarlenSmem)
-            tq *= 2;
-        g.TQ = (int)tq;
-        g.n_chunks = (int)ceil_div(N, tq);
-    }
+    const int W = g.W;
     StageTimer tm(T_VARLEN, s);
     cudaMemsetAsync(err, 0, sizeof(int), s);
     size_t hsmem = (size_t)g.n_blocks * sizeof(int);
@@ -772,7 +775,7 @@ static int run_varlen(const int32_t* topk, int64_t bh, int64_t N, int width, int
     }
     if (st) return st;
     if (W > 0) {
-        const size_t wsmem = wide_smem(g.TQ, W);
+        const size_t wsmem = varlen_wide_smem(g.TQ, W, g.n_blocks, width);
         switch (W) {
 #define MOBA_SCATTER_W(w)                                                                                       \
     case w:                                                                                                     \
@@ -864,15 +867,14 @@ static int dispatch_route_k(const void* q, bool q_f32, const float* cent, int64_
 using namespace moba;
 
 // workspace: [varlen: err | chunk counts] [route tc: bf16 centroid split 3 x bh x n x 128]
-static size_t varlen_ws_bytes(int64_t bh, int64_t n_tokens, int block_size) {
-    VarlenGeom g = varlen_geom(n_tokens, block_size);
+static size_t varlen_ws_bytes(int64_t bh, int64_t n_tokens, int block_size, int width) {
+    const VarlenGeom g = varlen_geom(bh, n_tokens, block_size, width);
     return align_up(256 + (size_t)bh * g.n_chunks * g.n_blocks * sizeof(int32_t), 1024);
 }
 
 extern "C" size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int block_size, int top_k) {
-    (void)top_k;
-    if (block_size < 1 || n_tokens < 1) return 0;
-    return varlen_ws_bytes(bh, n_tokens, block_size) + route_tc_ws_bytes(bh, n_tokens, block_size);
+    if (block_size < 1 || n_tokens < 1 || top_k < 0) return 0;
+    return varlen_ws_bytes(bh, n_tokens, block_size, top_k + 1) + route_tc_ws_bytes(bh, n_tokens, block_size);
 }
 
 static int route_impl(const void* q, bool q_f32, const float* centroids, int64_t bh, int kv_group, int64_t n_tokens,
@@ -890,7 +892,7 @@ static int route_impl(const void* q, bool q_f32, const float* centroids, int64_t
     {
     StageTimer tm(T_ROUTE, s);
     if (workspace_bytes < moba_route_workspace_size(bh, n_tokens, block_size, top_k)) return MOBA_ERR_WORKSPACE;
-    void* split_ws = (char*)workspace + varlen_ws_bytes(bh, n_tokens, block_size);
+    void* split_ws = (char*)workspace + varlen_ws_bytes(bh, n_tokens, block_size, top_k + 1);
     if (head_dim == 64)
         st = dispatch_route_k<64>(q, q_f32, centroids, bh, n_tokens, block_size, top_k, mode, kv_group, topk,
                                   split_ws, s);

@@ -65,24 +65,30 @@ def test_varlen_matches_oracle(H, N, B, width, causal):
         _check(topk[h], plan, h, n)
 
 
-def test_varlen_metric_point_torch_sort():
-    """64K x 8 heads of causal top-8 rows (the metric shape's plan geometry:
-    n = 512, 2 KB chunks): checked against a torch.sort of the (block,
-    query) pairs on the device."""
-    H, N, B, k = 8, 65536, 128, 8
-    g = torch.Generator(device="cuda").manual_seed(7)
+def _causal_topk(H, N, B, k, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
     own = torch.arange(N, device="cuda") // B
-    # k distinct past blocks per row (fewer near the start), sorted, then own
-    r = torch.rand(H, N, own.max().item() + 1, device="cuda", generator=g)
-    r = torch.where(torch.arange(r.shape[2], device="cuda")[None, None, :] < own[None, :, None], r, -1.0)
-    top = torch.topk(r, k, dim=2)
-    sel = torch.where(top.values >= 0, top.indices, torch.full_like(top.indices, 1 << 30))
-    sel = torch.sort(sel, dim=2).values
-    sel = torch.where(sel == (1 << 30), torch.full_like(sel, -1), sel)
-    topk = torch.cat([sel, own[None, :, None].expand(H, N, 1)], dim=2).int().contiguous()
-    del r
-    plan = _device.varlen(topk, B)
-    W = k + 1
+    n = int(own.max().item()) + 1
+    # k distinct past blocks per row (fewer near the start), sorted, then own;
+    # scores drawn per (row, block) in row slabs to bound memory
+    rows = []
+    for h in range(H):
+        sel_h = []
+        for r0 in range(0, N, 8192):
+            o = own[r0:r0 + 8192]
+            r = torch.rand(o.numel(), n, device="cuda", generator=g)
+            r = torch.where(torch.arange(n, device="cuda")[None, :] < o[:, None], r, -1.0)
+            top = torch.topk(r, min(k, n), dim=1)
+            sel = torch.where(top.values >= 0, top.indices, torch.full_like(top.indices, 1 << 30))
+            sel = torch.sort(sel, dim=1).values
+            sel_h.append(torch.where(sel == (1 << 30), torch.full_like(sel, -1), sel))
+        rows.append(torch.cat(sel_h))
+    sel = torch.stack(rows)
+    return torch.cat([sel, own[None, :, None].expand(H, N, 1)], dim=2).int().contiguous()
+
+
+def _check_torch_sort(topk, plan, B):
+    H, N, W = topk.shape
     for h in range(H):
         t = topk[h].reshape(-1).long()
         q = torch.arange(N, device="cuda").repeat_interleave(W)
@@ -95,3 +101,15 @@ def test_varlen_metric_point_torch_sort():
         rp[perm[:nv]] = torch.arange(nv, device="cuda")
         assert torch.equal(plan.row_pos[h].reshape(-1), rp.int())
         assert torch.equal(plan.counts_d[h], torch.bincount(t[ok], minlength=-(-N // B)).int())
+
+
+@pytest.mark.parametrize("H,N,B,k", [
+    (8, 65536, 128, 8),     # the metric shape's plan geometry: n = 512, 512-query chunks, 16 walking warps
+    (1, 524288, 32, 16),    # n = 16384, 17-wide rows: the cursor words do not fit, one-warp fallback
+])
+def test_varlen_causal_torch_sort(H, N, B, k):
+    """Causal top-k rows (the router's row format) against a torch.sort of
+    the (block, query) pairs on the device."""
+    topk = _causal_topk(H, N, B, k, seed=N + k)
+    plan = _device.varlen(topk, B)
+    _check_torch_sort(topk, plan, B)
