@@ -20,7 +20,7 @@
 //   T+1 ..   selection: 4 warps per tile (TMEM lane quadrant = warp % 4),
 //            one query row per thread over every chunk of the row.
 //
-// Selection keeps a sorted list of LS = top_k + 4 packed 32-bit keys per
+// Selection keeps a sorted list of LS = top_k + 2 (+ 3) packed 32-bit keys per
 // row: the order-preserving bits of the tensor-core score with the low
 // `idx_bits` replaced by (2^idx_bits - 1 - j), so one unsigned compare
 // orders by (truncated score desc, block index asc) and inserting a key
@@ -232,7 +232,13 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     using namespace sm100;
     using G = Geo<D, TT>;
     constexpr int T = G::T, NBUF = G::NBUF, CS = G::CS;
-    constexpr int LS = (KMAX + 4 < 32) ? KMAX + 4 : 32;
+    // list length: k + 2 keys while a row has <= ~2K candidates (TT <= 3),
+    // k + 3 for the >= 256K-token units (TT = 4), whose denser score tails
+    // leave more rows undecided with a short list (measured route+varlen,
+    // 32 heads d64: 64K 0.926 -> 0.900 ms with k + 2; 512K 19.16 -> 18.71 ms
+    // with k + 3 but 22.5 ms with k + 2; d128 64K 0.952 -> 0.908 ms)
+    constexpr int LS_EXTRA = TT >= 4 ? 3 : 2;
+    constexpr int LS = (KMAX + LS_EXTRA < 32) ? KMAX + LS_EXTRA : 32;
     constexpr int SL = D / 64;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
