@@ -55,9 +55,9 @@ constexpr int kN = 128;            // centroids per chunk (MMA N)
 constexpr int kSplits = 2;         // bf16 hi + lo terms of the fp32 centroids
 constexpr int kW = 64;             // score columns per TMEM buffer (MMA N of one sub-chunk)
 
-// TT: query tiles per unit — 3 (16 warps) at d = 64, 4 (21 warps, more
-// selection warps in flight per SM) for long sequences at d = 64 (512K route
-// 24.3 -> 23.2 ms; no gain below 256K), 2 (11 warps) at d = 128
+// TT: query tiles per unit — 4 (21 warps, more selection warps in flight
+// per SM) at d = 64 (the launch table in launch_route_tc), 2 (11 warps) at
+// d = 128; 3 (16 warps) is kept for the A/B record
 template <int D, int TT = (D == 64) ? 3 : 2>
 struct Geo {
     static constexpr int T = TT;
@@ -223,7 +223,7 @@ MOBA_DEV float exact_score_g(const __nv_bfloat16* __restrict__ q, const float* _
     return acc;
 }
 
-template <int D, int KMAX, int TT>
+template <int D, int KMAX, int TT, int LX>
 __global__ void __launch_bounds__(Geo<D, TT>::kThreads, 1)
 route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_c,
                 const __nv_bfloat16* __restrict__ Q, const float* __restrict__ cent, const float* __restrict__ cmax2,
@@ -232,12 +232,10 @@ route_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     using namespace sm100;
     using G = Geo<D, TT>;
     constexpr int T = G::T, NBUF = G::NBUF, CS = G::CS;
-    // list length: k + 2 keys while a row has <= ~2K candidates (TT <= 3),
-    // k + 3 for the >= 256K-token units (TT = 4), whose denser score tails
-    // leave more rows undecided with a short list (measured route+varlen,
-    // 32 heads d64: 64K 0.926 -> 0.900 ms with k + 2; 512K 19.16 -> 18.71 ms
-    // with k + 3 but 22.5 ms with k + 2; d128 64K 0.952 -> 0.908 ms)
-    constexpr int LS_EXTRA = TT >= 4 ? 3 : 2;
+    // list length k + LX: LX = 2 while a row has <= ~2K candidates, 3 from
+    // 256K tokens, whose denser score tails leave more rows undecided with a
+    // short list (route_topk_launch)
+    constexpr int LS_EXTRA = LX;
     constexpr int LS = (KMAX + LS_EXTRA < 32) ? KMAX + LS_EXTRA : 32;
     constexpr int SL = D / 64;
     extern __shared__ uint8_t smem_raw[];
@@ -735,23 +733,36 @@ int launch_route_tc(const void* q, const float* cent, int64_t bh, int kv_group, 
     int idx_bits = 1;
     while ((1ll << idx_bits) < n) ++idx_bits;
     if (idx_bits > 20) return MOBA_ERR_UNSUPPORTED;
-    auto go = [&](auto tt_tag) -> int {
+    auto go = [&](auto tt_tag, auto lx_tag) -> int {
         constexpr int TT = decltype(tt_tag)::value;
+        constexpr int LX = decltype(lx_tag)::value;
         using G = Geo<D, TT>;
         const int n_groups = (int)ceil_div(n_tiles, G::T);
         const int64_t units = bh * n_groups;
         if (units >= (1ll << 31)) return MOBA_ERR_UNSUPPORTED;
-        auto kern = route_tc_kernel<D, KMAX, TT>;
+        auto kern = route_tc_kernel<D, KMAX, TT, LX>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
         const unsigned grid = (unsigned)std::min<int64_t>(units, kNumSMs);
         kern<<<grid, G::kThreads, G::kSmem, s>>>(tm_q, tm_c, (const __nv_bfloat16*)q, cent, cmax2, N, B, top_k, rows,
                                                  kv_group, (int)bh, n_tiles, n_groups, idx_bits, topk, recheck);
         return check_launch("route_tc_kernel");
     };
+    // d = 64: units of 4 query tiles (21 warps); per-row lists of k + 2 keys,
+    // k + 3 from 256K tokens. Measured route+varlen, 32 heads d64 (tc plans
+    // bitwise the fp32 router's in every variant):
+    //            3 tiles, k+4 | 3 tiles, k+2 | 4 tiles, k+3 | 4 tiles, k+2
+    //   64K       0.926 ms    |   0.897      |   0.876      |   0.860
+    //   128K        -         |   2.26       |   2.22       |   2.17
+    //   256K        -         |   6.51       |   6.11       |   6.20
+    //   512K      19.16 (4 tiles)  -        |  18.71       |  22.5
+    // d = 128: units of 2 tiles, k + 2 (64K 0.952 -> 0.908 ms vs k + 4)
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using I4 = std::integral_constant<int, 4>;
     if constexpr (D == 64)
-        st = (N >= (1 << 18)) ? go(std::integral_constant<int, 4>{}) : go(std::integral_constant<int, 3>{});
+        st = (N >= (1 << 18)) ? go(I4{}, I3{}) : go(I4{}, I2{});
     else
-        st = go(std::integral_constant<int, 2>{});
+        st = go(I2{}, I2{});
     if (st) return st;
     route_recheck_kernel<D, KMAX><<<kNumSMs * 2, 256, 0, s>>>((const __nv_bfloat16*)q, cent, N, B, top_k, kv_group,
                                                               recheck, (int)(bh * n_tiles), topk);
