@@ -87,7 +87,9 @@ int moba_centroids_f32(const float* k, const float* conv_w, int conv_width,
                        int64_t bh, int64_t n_tokens, int head_dim, int block_size,
                        void* k_conv_out, float* centroids, void* stream);
 
-/* Workspace bytes needed by moba_route / moba_varlen. */
+/* Workspace bytes needed by moba_route / moba_varlen. The varlen chunk
+ * geometry depends on bh and the row width, so pass the call's top_k (for
+ * moba_varlen: width - 1); a smaller workspace returns MOBA_ERR_WORKSPACE. */
 size_t moba_route_workspace_size(int64_t bh, int64_t n_tokens, int block_size, int top_k);
 
 /*
